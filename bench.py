@@ -1,0 +1,304 @@
+#!/usr/bin/env python3
+"""Benchmark: rhs-blocked Wilson-Dirac apply on B200 (+ batched GMRES TTS).
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` prints
+ONE JSON line on rank 0.  ``--impl reference`` times the CPU oracle port of
+the reference path (lqcdlab is pure numpy) on the host cores.
+
+Workload at N=1 (BASELINE.json configs[1]): 16^3 x 32 lattice (T=32 slowest),
+seeded random SU(3) links (gen_gauge QR), Gaussian spinors, m0 = 0.1, C = 0,
+nrhs in {1,2,4,8,16,32}, complex128 and complex64.  Headline = c128 at
+nrhs=16 (site*rhs/s), every other (dtype, nrhs) point is in "sweep".  A step
+is one D_W apply of one nrhs block; steps rotate through enough distinct
+(psi, eta) buffer pairs that the bytes touched between two uses of a buffer
+exceed 4x the L2 size (no L2 reuse across steps).  Batched GMRES
+time-to-solution on BASELINE configs[3] (24^3 x 48, nrhs=12, near-unit
+links, antiperiodic T, GMRES(30), tol 1e-10, full and odd-even) is added
+under "gmres" unless --no-gmres.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CFG2_DIMS = (32, 16, 16, 16)
+SWEEP_B = (1, 2, 4, 8, 16, 32)
+HEADLINE = ("c128", 16)
+M0 = 0.1
+METRIC = "D_W apply site*rhs/s (16^3x32, nrhs=16, c128)"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int = 0):
+        self.gpu, self.samples, self._stop = gpu, [], threading.Event()
+        self._t = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---- GPU arm ------------------------------------------------------------------
+
+
+def gpu_sweep(args, torch, P):
+    from paper_2601_05816_b200 import _lib
+    from paper_2601_05816_b200.device import DeviceField, upload_gauge
+    from paper_2601_05816_b200.dirac import compulsory_bytes_per_site
+
+    dev = torch.device("cuda", 0)
+    geom = P.LatticeGeometry(CFG2_DIMS)
+    n = geom.n_sites
+    gauge = P.gen_gauge(geom, "random", seed=0)
+    _, l2 = _l2_bytes(_lib)
+    lat = _lib.Lattice.make(geom.dims)
+    gdev = {dt: upload_gauge(gauge, dt) for dt in ("c128", "c64")}
+    stream = torch.cuda.current_stream()
+    sptr = int(stream.cuda_stream)
+    results = []
+    hbm_peak, peak_kind = peaks()
+    for dt in ("c128", "c64"):
+        w = 16 if dt == "c128" else 8
+        for b in SWEEP_B:
+            field_bytes = n * 12 * b * w
+            nbuf = max(2, int(np.ceil(4 * l2 / (2 * field_bytes))) + 1)
+            g = torch.Generator(device="cpu").manual_seed(b)
+            base = torch.randn((12, n, b), dtype=torch.complex128, generator=g)
+            tdt = torch.complex128 if dt == "c128" else torch.complex64
+            psis = [DeviceField(base.to(dev, tdt)) for _ in range(nbuf)]
+            etas = [DeviceField(torch.empty_like(psis[0].data)) for _ in range(nbuf)]
+            code = 0 if dt == "c128" else 1
+
+            def launch(i):
+                rc = _lib.load().b200wd_dirac_apply(lat, code, b, M0, gdev[dt].ptr, psis[i % nbuf].ptr,
+                                                    etas[i % nbuf].ptr, sptr)
+                if rc:
+                    raise RuntimeError(_lib.load().b200wd_last_error().decode())
+
+            for i in range(max(3, args.warmup)):
+                launch(i)
+            torch.cuda.synchronize()
+            steps = args.steps
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+            ev[0].record(stream)
+            for i in range(steps):
+                launch(i)
+                ev[i + 1].record(stream)
+            torch.cuda.synchronize()
+            per = [ev[i].elapsed_time(ev[i + 1]) * 1e-3 for i in range(steps)]
+            t = float(np.mean(per))
+            alg = compulsory_bytes_per_site(b, dt) * n
+            results.append({"dtype": dt, "nrhs": b, "ms": t * 1e3, "site_rhs_per_s": n * b / t,
+                            "hbm_gbs": alg / t / 1e9, "frac": alg / t / 1e9 / hbm_peak, "bytes_per_launch": alg,
+                            "buffers": nbuf})
+            del psis, etas
+            torch.cuda.empty_cache()
+    return results, hbm_peak, peak_kind
+
+
+def _l2_bytes(_lib):
+    import ctypes
+    sm = ctypes.c_int32()
+    l2 = ctypes.c_int64()
+    _lib.call("b200wd_device_info", 0, ctypes.byref(sm), ctypes.byref(l2), None, None)
+    return sm.value, l2.value
+
+
+def gpu_e2e(args, torch, P, b=16, dt="c128"):
+    """Same metric through the public API with pinned host buffers."""
+    geom = P.LatticeGeometry(CFG2_DIMS)
+    n = geom.n_sites
+    gauge = P.gen_gauge(geom, "random", seed=0)
+    params = P.DiracParams(m0=M0)
+    h_in = torch.empty(n * 12 * b, dtype=torch.complex128).pin_memory()
+    h_out = torch.empty(n * 12 * b, dtype=torch.complex128).pin_memory()
+    h_in.copy_(torch.randn(n * 12 * b, dtype=torch.complex128))
+    psi = P.BlockSpinorField(n, 12, b, P.Layout.COMPONENT_MAJOR, h_in.numpy(), geom)
+    eta = P.BlockSpinorField(n, 12, b, P.Layout.COMPONENT_MAJOR, h_out.numpy(), geom)
+    for _ in range(max(3, args.warmup)):
+        P.apply_dirac(params, gauge, None, psi, dtype=dt, out=eta)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        P.apply_dirac(params, gauge, None, psi, dtype=dt, out=eta)
+    torch.cuda.synchronize()
+    t = (time.perf_counter() - t0) / args.steps
+    return {"value": n * b / t, "unit": "site*rhs/s", "h2d_bytes_per_step": n * 12 * b * 16,
+            "d2h_bytes_per_step": n * 12 * b * 16, "ms_per_step": t * 1e3}
+
+
+def gpu_gmres(args, torch, P):
+    """BASELINE configs[3]: GMRES(30) b=12 tol 1e-10 on 24^3 x 48, full and odd-even."""
+    dims = (48, 24, 24, 24)
+    geom = P.LatticeGeometry(dims)
+    t0 = time.perf_counter()
+    gauge = P.flip_time_boundary(P.near_unit_gauge(geom, 0.3, 3))
+    eta = P.gen_spinor(geom.n_sites, 12, P.Layout.COMPONENT_MAJOR, seed=5, geom=geom)
+    gen_s = time.perf_counter() - t0
+    from paper_2601_05816_b200.device import upload
+    d_eta = upload(eta)
+    cfg = P.GmresConfig(restart_len=30, restarts=67, tol=1e-10)
+    out = {"lattice": list(dims), "nrhs": 12, "input_gen_s": gen_s}
+    for oe in (False, True):
+        P.solve_dirac(P.DiracParams(m0=M0), gauge, None, d_eta,
+                      P.GmresConfig(restart_len=2, restarts=1, tol=1e-10), odd_even=oe)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = P.solve_dirac(P.DiracParams(m0=M0), gauge, None, d_eta, cfg, odd_even=oe)
+        torch.cuda.synchronize()
+        tts = time.perf_counter() - t0
+        out["oe" if oe else "full"] = {"iterations": rep.iterations, "time_to_solution_s": tts,
+                                       "s_per_iteration": tts / max(rep.iterations, 1),
+                                       "max_full_relnorm": float(rep.full_relnorms.max())}
+    return out
+
+
+def cpu_baseline_sample(b=16, reps=3):
+    """Oracle port (numpy restatement of lqcdlab) on a 16^3 x 2 slab sample."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import lqcd_oracle as O
+    dims = (2, 16, 16, 16)
+    n = 2 * 16 ** 3
+    links = O.gen_gauge_random(dims, 0)
+    psi = O.gen_spinor(n, b, 2)
+    with threadpool_limits(1):
+        O.apply_dirac(dims, M0, links, None, psi)
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            O.apply_dirac(dims, M0, links, None, psi)
+            ts.append(time.perf_counter() - t0)
+    t = float(np.median(ts))
+    return {"value": n * b / t, "unit": "site*rhs/s", "cores": 1, "kind": "port",
+            "sample": f"oracle apply_dirac on a 16^3x2 slab (8192 sites), nrhs={b}, c128, median of {reps}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-gmres", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return reference_arm(args)
+    import torch
+    import paper_2601_05816_b200 as P
+    torch.cuda.set_device(0)
+    clocks = ClockSampler(0).start()
+    sweep, hbm_peak, peak_kind = gpu_sweep(args, torch, P)
+    clk = clocks.stop()
+    head = next(r for r in sweep if (r["dtype"], r["nrhs"]) == HEADLINE)
+    e2e = gpu_e2e(args, torch, P)
+    line = {
+        "metric": METRIC, "value": head["site_rhs_per_s"], "unit": "site*rhs/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded SU(3) links, Gaussian rhs)",
+        "config": {"workload": "BASELINE configs[1]: D_W apply 16^3x32, nrhs sweep {1..32}, c128+c64; headline c128 nrhs=16",
+                   "lattice": list(CFG2_DIMS), "nrhs": 16, "m0": M0, "l2": "rotating buffers > 4x L2 between reuses",
+                   "parallelism": "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": head["hbm_gbs"], "peak": hbm_peak, "unit": "GB/s",
+                     "frac": head["frac"], "traffic": None, "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": head["bytes_per_launch"]},
+        "e2e": e2e, "gpu_launches": args.steps, "clocks": clk,
+        "sweep": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()} for r in sweep],
+    }
+    if not args.no_gmres:
+        line["gmres"] = gpu_gmres(args, torch, P)
+    if not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline_sample()
+    print(json.dumps(line))
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    b = HEADLINE[1]
+    from threadpoolctl import threadpool_limits
+
+    from oracle import lqcd_oracle as O
+    dims = (2, 16, 16, 16)
+    n = 2 * 16 ** 3
+    links = O.gen_gauge_random(dims, 0)
+    psi = O.gen_spinor(n, b, 2)
+    cores = os.cpu_count() or 1
+    with threadpool_limits(cores):
+        for _ in range(args.warmup):
+            O.apply_dirac(dims, M0, links, None, psi)
+        ts = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            O.apply_dirac(dims, M0, links, None, psi)
+            ts.append(time.perf_counter() - t0)
+    t = float(np.mean(ts))
+    v = n * b / t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "site*rhs/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": "BASELINE configs[1] sample: 16^3x2 slab of the 16^3x32 lattice, nrhs=16, c128",
+                       "lattice": [2, 16, 16, 16], "nrhs": b, "m0": M0},
+            "cpu_baseline": {"value": v, "unit": "site*rhs/s", "cores": cores, "kind": "port",
+                             "sample": "oracle (numpy port of lqcdlab apply_dirac) on a 16^3x2 slab, 8192 sites"},
+            "e2e": {"value": v, "unit": "site*rhs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

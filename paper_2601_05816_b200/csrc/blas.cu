@@ -1,0 +1,510 @@
+// Per-rhs BLAS-1 and the batched-GMRES Arnoldi kernels (complex128 planes).
+//
+// Reductions are lane-per-rhs: a block is (b, S) threads, thread (r, y)
+// owns rhs r and walks sites y, y+S*G, ... in a fixed order, so every rhs
+// sees an identical summation tree (replicated right-hand sides give
+// bit-identical histories, tests/test_gmres.py:141-151).  Block partials go
+// to scratch; the last block to finish (atomic ticket) folds them in a fixed
+// order -- the result is deterministic run to run.  The GMRES kernels fuse
+// each MGS axpy with the next inner product (or the final norm), keep the
+// basis unnormalised (V_p = sigma_p Z_p) so no separate normalise pass is
+// needed, and run the Givens/least-squares bookkeeping on the device with
+// one thread per rhs (gmres.py:101-177).
+#include <math.h>
+
+#include "capi.cuh"
+#include "common.cuh"
+
+namespace b200wd {
+
+constexpr int kMaxGrid = 148 * 4;
+constexpr int kBlock = 256;
+
+static inline int rows_per_block(int b) { return b >= kBlock ? 1 : kBlock / b; }
+
+static inline int grid_for_sites(int64_t n, int S) {
+  int64_t g = (n + S - 1) / S;
+  if (g > kMaxGrid) g = kMaxGrid;
+  return (int)(g < 1 ? 1 : g);
+}
+
+struct Scratch {
+  double2* partials;  // [kMaxGrid][b]
+  unsigned* ticket;
+};
+static inline Scratch scratch_of(void* p, int b) {
+  Scratch s;
+  s.partials = static_cast<double2*>(p);
+  s.ticket = reinterpret_cast<unsigned*>(static_cast<char*>(p) + (size_t)kMaxGrid * b * sizeof(double2));
+  return s;
+}
+
+// Block-reduce `v` over threadIdx.y (fixed tree), write the block partial,
+// and let the last block fold all partials into out[r].
+__device__ void reduce_finish(double2 v, Scratch sc, double2* out) {
+  extern __shared__ double2 red[];  // [S][b]
+  const int b = blockDim.x, S = blockDim.y, r = threadIdx.x, y = threadIdx.y;
+  __shared__ unsigned s_last;
+  red[y * b + r] = v;
+  __syncthreads();
+  int p2 = 1;
+  while (p2 < S) p2 <<= 1;
+  for (int stride = p2 >> 1; stride > 0; stride >>= 1) {
+    if (y < stride && y + stride < S) {
+      double2 a = red[y * b + r], c = red[(y + stride) * b + r];
+      red[y * b + r] = make_double2(a.x + c.x, a.y + c.y);
+    }
+    __syncthreads();
+  }
+  if (y == 0) sc.partials[(size_t)blockIdx.x * b + r] = red[r];
+  __threadfence();
+  __syncthreads();
+  if (r == 0 && y == 0) s_last = (atomicAdd(sc.ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double2 acc = make_double2(0.0, 0.0);
+  for (int g = y; g < (int)gridDim.x; g += S) {
+    double2 q = __ldcg(sc.partials + (size_t)g * b + r);
+    acc.x += q.x;
+    acc.y += q.y;
+  }
+  red[y * b + r] = acc;
+  __syncthreads();
+  for (int stride = p2 >> 1; stride > 0; stride >>= 1) {
+    if (y < stride && y + stride < S) {
+      double2 a = red[y * b + r], c = red[(y + stride) * b + r];
+      red[y * b + r] = make_double2(a.x + c.x, a.y + c.y);
+    }
+    __syncthreads();
+  }
+  if (y == 0) {
+    out[r] = red[r];
+    if (r == 0) *sc.ticket = 0u;
+  }
+}
+
+__device__ __forceinline__ void acc_dot(double2& a, double2 x, double2 y) {
+  // conj(x) * y
+  a.x = fma(x.x, y.x, a.x);
+  a.x = fma(x.y, y.y, a.x);
+  a.y = fma(x.x, y.y, a.y);
+  a.y = fma(-x.y, y.x, a.y);
+}
+
+// ---- reference BLAS ----------------------------------------------------------
+__global__ void dot_kernel(int64_t n, int s, const double2* __restrict__ x, const double2* __restrict__ yv,
+                           double2* out, Scratch sc) {
+  const int b = blockDim.x, r = threadIdx.x;
+  double2 a = make_double2(0.0, 0.0);
+  for (int64_t site = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; site < n;
+       site += (int64_t)gridDim.x * blockDim.y)
+    for (int k = 0; k < s; ++k) {
+      const int64_t i = ((int64_t)k * n + site) * b + r;
+      acc_dot(a, __ldg(x + i), __ldg(yv + i));
+    }
+  reduce_finish(a, sc, out);
+}
+
+__global__ void norm2_kernel(int64_t n, int s, const double2* __restrict__ x, double2* out, Scratch sc) {
+  const int b = blockDim.x, r = threadIdx.x;
+  double2 a = make_double2(0.0, 0.0);
+  for (int64_t site = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; site < n;
+       site += (int64_t)gridDim.x * blockDim.y)
+    for (int k = 0; k < s; ++k) {
+      const double2 v = __ldg(x + ((int64_t)k * n + site) * b + r);
+      a.x = fma(v.x, v.x, a.x);
+      a.x = fma(v.y, v.y, a.x);
+    }
+  reduce_finish(a, sc, out);
+}
+
+__global__ void axpy_kernel(int64_t total, int b, const double2* __restrict__ alpha, const double2* __restrict__ x,
+                            double2* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 a = __ldg(alpha + i % b);
+    y[i] = cmac(y[i], a, __ldg(x + i));
+  }
+}
+
+__global__ void scale_kernel(int64_t total, int b, const double2* __restrict__ alpha, double2* __restrict__ x) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = cmul(__ldg(alpha + i % b), x[i]);
+}
+
+// ---- GMRES ------------------------------------------------------------------
+struct GState {
+  int b, m;
+  double brk_rel;
+  double2 *h_raw, *h, *gamma, *sn, *dot, *y;
+  double *cs, *sigma, *eta_norm, *relnorm;
+  int* brk;
+  Scratch sc;
+};
+
+static GState gstate(const b200wd_gmres_state* st) {
+  GState g;
+  g.b = st->b;
+  g.m = st->m;
+  g.brk_rel = st->breakdown_rel;
+  g.h_raw = static_cast<double2*>(st->h_raw);
+  g.h = static_cast<double2*>(st->h);
+  g.gamma = static_cast<double2*>(st->gamma);
+  g.sn = static_cast<double2*>(st->sn);
+  g.dot = static_cast<double2*>(st->dot);
+  g.y = static_cast<double2*>(st->y);
+  g.cs = static_cast<double*>(st->cs);
+  g.sigma = static_cast<double*>(st->sigma);
+  g.eta_norm = static_cast<double*>(st->eta_norm);
+  g.relnorm = static_cast<double*>(st->relnorm);
+  g.brk = static_cast<int*>(st->breakdown);
+  g.sc = scratch_of(st->scratch, st->b);
+  return g;
+}
+
+constexpr double kTiny = 1e-300;  // gmres.py:39
+
+__device__ __forceinline__ double cabs_(double2 a) { return hypot(a.x, a.y); }
+
+// r := eta - r ; dot := ||r||^2
+__global__ void residual_kernel(int64_t n, int s, const double2* __restrict__ eta, double2* __restrict__ r,
+                                GState g) {
+  const int b = blockDim.x, rr = threadIdx.x;
+  double2 a = make_double2(0.0, 0.0);
+  for (int64_t site = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; site < n;
+       site += (int64_t)gridDim.x * blockDim.y)
+    for (int k = 0; k < s; ++k) {
+      const int64_t i = ((int64_t)k * n + site) * b + rr;
+      const double2 e = __ldg(eta + i), v = r[i];
+      const double2 d = make_double2(e.x - v.x, e.y - v.y);
+      r[i] = d;
+      a.x = fma(d.x, d.x, a.x);
+      a.x = fma(d.y, d.y, a.x);
+    }
+  reduce_finish(a, g.sc, g.dot);
+}
+
+// eta_norm = sqrt(dot), breakdown flags cleared (gmres.py:204-205)
+__global__ void init_kernel(GState g) {
+  const int r = threadIdx.x;
+  if (r >= g.b) return;
+  g.eta_norm[r] = sqrt(g.dot[r].x);
+  g.brk[r] = 0;
+}
+
+// cycle start (gmres.py:180-198)
+__global__ void start_kernel(GState g) {
+  const int r = threadIdx.x;
+  if (r >= g.b) return;
+  const int m = g.m;
+  const double beta = sqrt(g.dot[r].x);
+  for (int i = 0; i < (m + 1) * m; ++i) {
+    g.h[(size_t)r * (m + 1) * m + i] = make_double2(0.0, 0.0);
+    g.h_raw[(size_t)r * (m + 1) * m + i] = make_double2(0.0, 0.0);
+  }
+  for (int i = 0; i <= m; ++i) g.gamma[(size_t)r * (m + 1) + i] = make_double2(0.0, 0.0);
+  for (int i = 0; i < m; ++i) {
+    g.cs[(size_t)r * m + i] = 0.0;
+    g.sn[(size_t)r * m + i] = make_double2(0.0, 0.0);
+  }
+  for (int i = 0; i <= m; ++i) g.sigma[(size_t)i * g.b + r] = 0.0;
+  g.gamma[(size_t)r * (m + 1)] = make_double2(beta, 0.0);
+  g.sigma[r] = beta > 0 ? 1.0 / beta : 0.0;
+  const double en = g.eta_norm[r];
+  g.relnorm[r] = en > 0 ? beta / fmax(en, kTiny) : 0.0;
+}
+
+// dot := <Z, w>
+__global__ void gdot_kernel(int64_t n, int s, const double2* __restrict__ z, const double2* __restrict__ w, GState g) {
+  const int b = blockDim.x, r = threadIdx.x;
+  double2 a = make_double2(0.0, 0.0);
+  for (int64_t site = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; site < n;
+       site += (int64_t)gridDim.x * blockDim.y)
+    for (int k = 0; k < s; ++k) {
+      const int64_t i = ((int64_t)k * n + site) * b + r;
+      acc_dot(a, __ldg(z + i), __ldg(w + i));
+    }
+  reduce_finish(a, g.sc, g.dot);
+}
+
+// fused MGS pass p of column j (gmres.py:118-121)
+template <bool NEXT>
+__global__ void mgs_kernel(int j, int p, int64_t n, int s, double2* __restrict__ w, const double2* __restrict__ zp,
+                           const double2* __restrict__ zn, GState g) {
+  const int b = blockDim.x, r = threadIdx.x;
+  const int m = g.m;
+  const double sig = g.sigma[(size_t)p * g.b + r];
+  const double2 d = g.dot[r];
+  const double2 hp = make_double2(sig * d.x, sig * d.y);  // h_p = <V_p, w>
+  const double2 c = make_double2(-sig * hp.x, -sig * hp.y);  // w -= h_p V_p = h_p sigma_p Z_p
+  if (blockIdx.x == 0 && threadIdx.y == 0) g.h_raw[((size_t)r * (m + 1) + p) * m + j] = hp;
+  double2 a = make_double2(0.0, 0.0);
+  for (int64_t site = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; site < n;
+       site += (int64_t)gridDim.x * blockDim.y)
+    for (int k = 0; k < s; ++k) {
+      const int64_t i = ((int64_t)k * n + site) * b + r;
+      const double2 wn = cmac(w[i], c, __ldg(zp + i));
+      w[i] = wn;
+      if (NEXT) {
+        acc_dot(a, __ldg(zn + i), wn);
+      } else {
+        a.x = fma(wn.x, wn.x, a.x);
+        a.x = fma(wn.y, wn.y, a.x);
+      }
+    }
+  reduce_finish(a, g.sc, g.dot);
+}
+
+// Givens pair (gmres.py:101-112): c real, s = phase(a) conj(b) / rho
+__device__ void givens(double2 a, double2 bb, double& c, double2& s) {
+  const double aa = cabs_(a), ab = cabs_(bb);
+  const double rho = sqrt(aa * aa + ab * ab);
+  if (rho > 0) {
+    c = aa > 0 ? aa / rho : 0.0;
+    const double2 ph = aa > 0 ? make_double2(a.x / aa, a.y / aa) : make_double2(1.0, 0.0);
+    const double2 t = cmul(ph, make_double2(bb.x, -bb.y));
+    s = make_double2(t.x / rho, t.y / rho);
+  } else {
+    c = 1.0;
+    s = make_double2(0.0, 0.0);
+  }
+}
+
+// close column j (gmres.py:135-157)
+__global__ void close_column_kernel(int j, GState g) {
+  const int r = threadIdx.x;
+  if (r >= g.b) return;
+  const int m = g.m;
+  const double hn = sqrt(g.dot[r].x);
+  const double en = g.eta_norm[r];
+  int brk = g.brk[r] | (hn <= g.brk_rel * en ? 1 : 0);
+  g.brk[r] = brk;
+  double2* hraw = g.h_raw + (size_t)r * (m + 1) * m;
+  double2* hh = g.h + (size_t)r * (m + 1) * m;
+  hraw[(j + 1) * m + j] = make_double2(brk ? 0.0 : hn, 0.0);
+  g.sigma[(size_t)(j + 1) * g.b + r] = (brk || hn <= 0) ? 0.0 : 1.0 / hn;
+  // fold the new column through the stored rotations
+  double2 col[2];
+  col[0] = hraw[0 * m + j];
+  double* cs = g.cs + (size_t)r * m;
+  double2* sn = g.sn + (size_t)r * m;
+  for (int p = 0; p < j; ++p) {
+    const double2 a0 = col[0], a1 = hraw[(p + 1) * m + j];
+    const double2 sp = sn[p];
+    const double2 t0 = cmul(sp, a1);
+    const double2 top = make_double2(cs[p] * a0.x + t0.x, cs[p] * a0.y + t0.y);
+    const double2 t1 = cmul(make_double2(-sp.x, sp.y), a0);  // -conj(s) a0
+    col[0] = make_double2(t1.x + cs[p] * a1.x, t1.y + cs[p] * a1.y);
+    hh[p * m + j] = top;
+  }
+  col[1] = hraw[(j + 1) * m + j];
+  double c;
+  double2 s;
+  givens(col[0], col[1], c, s);
+  cs[j] = c;
+  sn[j] = s;
+  const double2 t = cmul(s, col[1]);
+  hh[j * m + j] = make_double2(c * col[0].x + t.x, c * col[0].y + t.y);
+  hh[(j + 1) * m + j] = make_double2(0.0, 0.0);
+  double2* gam = g.gamma + (size_t)r * (m + 1);
+  const double2 gj = gam[j];
+  gam[j + 1] = cmul(make_double2(-s.x, s.y), gj);
+  gam[j] = make_double2(c * gj.x, c * gj.y);
+  g.relnorm[r] = en > 0 ? cabs_(gam[j + 1]) / fmax(en, kTiny) : 0.0;
+}
+
+// back substitution (gmres.py:161-177)
+__global__ void backsub_kernel(int jd, GState g) {
+  const int r = threadIdx.x;
+  if (r >= g.b) return;
+  const int m = g.m;
+  const double2* hh = g.h + (size_t)r * (m + 1) * m;
+  const double2* gam = g.gamma + (size_t)r * (m + 1);
+  double2* y = g.y + (size_t)r * m;
+  for (int row = jd - 1; row >= 0; --row) {
+    double2 acc = gam[row];
+    for (int c2 = row + 1; c2 < jd; ++c2) {
+      const double2 t = cmul(hh[row * m + c2], y[c2]);
+      acc.x -= t.x;
+      acc.y -= t.y;
+    }
+    const double2 dg = hh[row * m + row];
+    if (cabs_(dg) > 0) {
+      // acc / dg
+      const double den = dg.x * dg.x + dg.y * dg.y;
+      y[row] = make_double2((acc.x * dg.x + acc.y * dg.y) / den, (acc.y * dg.x - acc.x * dg.y) / den);
+    } else {
+      y[row] = make_double2(0.0, 0.0);
+    }
+  }
+}
+
+constexpr int kMaxBasis = 64;
+struct ZList {
+  const double2* z[kMaxBasis];
+};
+
+// psi += sum_p y_p sigma_p Z_p  (one pass over psi and the basis)
+__global__ void update_kernel(int jd, int64_t n, int s, ZList zl, double2* __restrict__ psi, GState g) {
+  const int b = blockDim.x, r = threadIdx.x;
+  const int m = g.m;
+  double2 coef[kMaxBasis];
+#pragma unroll 1
+  for (int p = 0; p < jd; ++p) {
+    const double2 yp = g.y[(size_t)r * m + p];
+    const double sg = g.sigma[(size_t)p * g.b + r];
+    coef[p] = make_double2(yp.x * sg, yp.y * sg);
+  }
+  for (int64_t site = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; site < n;
+       site += (int64_t)gridDim.x * blockDim.y)
+    for (int k = 0; k < s; ++k) {
+      const int64_t i = ((int64_t)k * n + site) * b + r;
+      double2 a = psi[i];
+#pragma unroll 1
+      for (int p = 0; p < jd; ++p) a = cmac(a, coef[p], __ldg(zl.z[p] + i));
+      psi[i] = a;
+    }
+}
+
+static dim3 red_block(int b) { return dim3(b, rows_per_block(b)); }
+static size_t red_smem(int b) { return (size_t)b * rows_per_block(b) * sizeof(double2); }
+
+}  // namespace b200wd
+
+using namespace b200wd;
+
+extern "C" int64_t b200wd_reduce_scratch_bytes(int32_t b) {
+  return (int64_t)kMaxGrid * b * (int64_t)sizeof(double2) + 64;
+}
+
+#define CHECK_FIELD(n, s, b)                                                                        \
+  B200WD_REQUIRE((n) >= 1 && (s) >= 1 && (b) >= 1 && (b) <= kBlock, "bad field shape n=%lld s=%d b=%d", \
+                 (long long)(n), (s), (b))
+
+extern "C" int b200wd_block_dot(int64_t n_sites, int32_t s, int32_t b, const void* x, const void* y, void* out,
+                                void* scratch, void* stream) {
+  CHECK_FIELD(n_sites, s, b);
+  B200WD_REQUIRE(x && y && out && scratch, "NULL pointer");
+  dim3 blk = red_block(b);
+  dot_kernel<<<grid_for_sites(n_sites, blk.y), blk, red_smem(b), as_stream(stream)>>>(
+      n_sites, s, static_cast<const double2*>(x), static_cast<const double2*>(y), static_cast<double2*>(out),
+      scratch_of(scratch, b));
+  return check_launch("b200wd_block_dot");
+}
+
+extern "C" int b200wd_block_norm2(int64_t n_sites, int32_t s, int32_t b, const void* x, void* out, void* scratch,
+                                  void* stream) {
+  CHECK_FIELD(n_sites, s, b);
+  B200WD_REQUIRE(x && out && scratch, "NULL pointer");
+  dim3 blk = red_block(b);
+  norm2_kernel<<<grid_for_sites(n_sites, blk.y), blk, red_smem(b), as_stream(stream)>>>(
+      n_sites, s, static_cast<const double2*>(x), static_cast<double2*>(out), scratch_of(scratch, b));
+  return check_launch("b200wd_block_norm2");
+}
+
+extern "C" int b200wd_block_axpy(int64_t n_sites, int32_t s, int32_t b, const void* alpha, const void* x, void* y,
+                                 void* stream) {
+  CHECK_FIELD(n_sites, s, b);
+  B200WD_REQUIRE(alpha && x && y, "NULL pointer");
+  const int64_t total = n_sites * s * b;
+  int64_t g = (total + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  axpy_kernel<<<(unsigned)g, 256, 0, as_stream(stream)>>>(total, b, static_cast<const double2*>(alpha),
+                                                          static_cast<const double2*>(x), static_cast<double2*>(y));
+  return check_launch("b200wd_block_axpy");
+}
+
+extern "C" int b200wd_block_scale(int64_t n_sites, int32_t s, int32_t b, const void* alpha, void* x, void* stream) {
+  CHECK_FIELD(n_sites, s, b);
+  B200WD_REQUIRE(alpha && x, "NULL pointer");
+  const int64_t total = n_sites * s * b;
+  int64_t g = (total + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  scale_kernel<<<(unsigned)g, 256, 0, as_stream(stream)>>>(total, b, static_cast<const double2*>(alpha),
+                                                           static_cast<double2*>(x));
+  return check_launch("b200wd_block_scale");
+}
+
+#define CHECK_STATE(st)                                                                        \
+  B200WD_REQUIRE((st) != nullptr && (st)->b >= 1 && (st)->b <= kBlock && (st)->m >= 1 &&      \
+                     (st)->m <= kMaxBasis - 1,                                                 \
+                 "bad GMRES state (b must be in [1,%d], restart length in [1,%d])", kBlock, \
+                 kMaxBasis - 1)
+
+extern "C" int b200wd_gmres_residual(const b200wd_gmres_state* st, int64_t n_sites, int32_t s, const void* eta,
+                                     void* r, void* stream) {
+  CHECK_STATE(st);
+  CHECK_FIELD(n_sites, s, st->b);
+  B200WD_REQUIRE(eta && r, "NULL pointer");
+  dim3 blk = red_block(st->b);
+  residual_kernel<<<grid_for_sites(n_sites, blk.y), blk, red_smem(st->b), as_stream(stream)>>>(
+      n_sites, s, static_cast<const double2*>(eta), static_cast<double2*>(r), gstate(st));
+  return check_launch("b200wd_gmres_residual");
+}
+
+extern "C" int b200wd_gmres_init(const b200wd_gmres_state* st, void* stream) {
+  CHECK_STATE(st);
+  init_kernel<<<1, st->b, 0, as_stream(stream)>>>(gstate(st));
+  return check_launch("b200wd_gmres_init");
+}
+
+extern "C" int b200wd_gmres_start(const b200wd_gmres_state* st, void* stream) {
+  CHECK_STATE(st);
+  start_kernel<<<1, st->b, 0, as_stream(stream)>>>(gstate(st));
+  return check_launch("b200wd_gmres_start");
+}
+
+extern "C" int b200wd_gmres_dot(const b200wd_gmres_state* st, int64_t n_sites, int32_t s, const void* z,
+                                const void* w, void* stream) {
+  CHECK_STATE(st);
+  CHECK_FIELD(n_sites, s, st->b);
+  B200WD_REQUIRE(z && w, "NULL pointer");
+  dim3 blk = red_block(st->b);
+  gdot_kernel<<<grid_for_sites(n_sites, blk.y), blk, red_smem(st->b), as_stream(stream)>>>(
+      n_sites, s, static_cast<const double2*>(z), static_cast<const double2*>(w), gstate(st));
+  return check_launch("b200wd_gmres_dot");
+}
+
+extern "C" int b200wd_gmres_mgs(const b200wd_gmres_state* st, int32_t j, int32_t p, int64_t n_sites, int32_t s,
+                                void* w, const void* z_p, const void* z_next, void* stream) {
+  CHECK_STATE(st);
+  CHECK_FIELD(n_sites, s, st->b);
+  B200WD_REQUIRE(0 <= p && p <= j && j < st->m, "MGS index p=%d j=%d outside restart length %d", p, j, st->m);
+  B200WD_REQUIRE(w && z_p, "NULL pointer");
+  dim3 blk = red_block(st->b);
+  const int grid = grid_for_sites(n_sites, blk.y);
+  if (z_next)
+    mgs_kernel<true><<<grid, blk, red_smem(st->b), as_stream(stream)>>>(
+        j, p, n_sites, s, static_cast<double2*>(w), static_cast<const double2*>(z_p),
+        static_cast<const double2*>(z_next), gstate(st));
+  else
+    mgs_kernel<false><<<grid, blk, red_smem(st->b), as_stream(stream)>>>(
+        j, p, n_sites, s, static_cast<double2*>(w), static_cast<const double2*>(z_p), nullptr, gstate(st));
+  return check_launch("b200wd_gmres_mgs");
+}
+
+extern "C" int b200wd_gmres_close_column(const b200wd_gmres_state* st, int32_t j, void* stream) {
+  CHECK_STATE(st);
+  B200WD_REQUIRE(0 <= j && j < st->m, "column %d outside restart length %d", j, st->m);
+  close_column_kernel<<<1, st->b, 0, as_stream(stream)>>>(j, gstate(st));
+  return check_launch("b200wd_gmres_close_column");
+}
+
+extern "C" int b200wd_gmres_update(const b200wd_gmres_state* st, int32_t j_done, int64_t n_sites, int32_t s,
+                                   const void* const* z, void* psi, void* stream) {
+  CHECK_STATE(st);
+  CHECK_FIELD(n_sites, s, st->b);
+  B200WD_REQUIRE(0 <= j_done && j_done <= st->m, "j_done=%d outside [0,%d]", j_done, st->m);
+  B200WD_REQUIRE(psi && (j_done == 0 || z), "NULL pointer");
+  if (j_done == 0) return B200WD_OK;
+  ZList zl{};
+  for (int p = 0; p < j_done; ++p) {
+    B200WD_REQUIRE(z[p] != nullptr, "basis pointer %d is NULL", p);
+    zl.z[p] = static_cast<const double2*>(z[p]);
+  }
+  backsub_kernel<<<1, st->b, 0, as_stream(stream)>>>(j_done, gstate(st));
+  dim3 blk = red_block(st->b);
+  update_kernel<<<grid_for_sites(n_sites, blk.y), blk, 0, as_stream(stream)>>>(
+      j_done, n_sites, s, zl, static_cast<double2*>(psi), gstate(st));
+  return check_launch("b200wd_gmres_update");
+}

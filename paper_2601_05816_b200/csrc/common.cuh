@@ -1,0 +1,109 @@
+// Shared device helpers for libb200wd (sm_100a only).
+//
+// Complex numbers are double2 (c128) or float2 (c64).  For c64 the complex
+// multiply-accumulate uses the Blackwell packed FP32 pipe (fma.rn.f32x2 ->
+// SASS FFMA2): (re,im) of one complex number ride in one 64-bit register
+// pair, the link entry is broadcast as a scalar, so one complex MAC is two
+// FFMA2 instead of four FFMA.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libb200wd targets sm_100a only"
+#endif
+
+namespace b200wd {
+
+template <typename R> struct cx_t;
+template <> struct cx_t<double> { using type = double2; };
+template <> struct cx_t<float>  { using type = float2; };
+template <typename R> using cx = typename cx_t<R>::type;
+
+__device__ __forceinline__ double2 mk(double a, double b) { return make_double2(a, b); }
+__device__ __forceinline__ float2  mk(float a, float b)  { return make_float2(a, b); }
+
+// ---- packed f32x2 helpers (PTX ISA 8.6+, sm_100+) --------------------------
+__device__ __forceinline__ unsigned long long pk(float2 a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ float2 upk(unsigned long long r) {
+  float2 o;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+  return o;
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)), "l"(pk(c)));
+  return upk(r);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+  return upk(r);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+  return upk(r);
+}
+
+// ---- complex arithmetic ----------------------------------------------------
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return mk(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return mk(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return add2(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return sub2(a, b); }
+
+// acc + u*h
+__device__ __forceinline__ double2 cmac(double2 acc, double2 u, double2 h) {
+  acc.x = fma(u.x, h.x, acc.x);
+  acc.x = fma(-u.y, h.y, acc.x);
+  acc.y = fma(u.x, h.y, acc.y);
+  acc.y = fma(u.y, h.x, acc.y);
+  return acc;
+}
+// acc + conj(u)*h
+__device__ __forceinline__ double2 cmacc(double2 acc, double2 u, double2 h) {
+  acc.x = fma(u.x, h.x, acc.x);
+  acc.x = fma(u.y, h.y, acc.x);
+  acc.y = fma(u.x, h.y, acc.y);
+  acc.y = fma(-u.y, h.x, acc.y);
+  return acc;
+}
+// float: hs = i*h = (-h.y, h.x) is formed once per h and reused for 3 rows
+__device__ __forceinline__ float2 cmac_s(float2 acc, float2 u, float2 h, float2 hs) {
+  acc = fma2(mk(u.x, u.x), h, acc);
+  return fma2(mk(u.y, u.y), hs, acc);
+}
+// conj(u)*h = u.x*h - u.y*(i h)
+__device__ __forceinline__ float2 cmacc_s(float2 acc, float2 u, float2 h, float2 hs) {
+  acc = fma2(mk(u.x, u.x), h, acc);
+  return fma2(mk(-u.y, -u.y), hs, acc);
+}
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+template <typename C> __device__ __forceinline__ C cscale(C a, decltype(a.x) s) { return mk(a.x * s, a.y * s); }
+template <typename C> __device__ __forceinline__ C cconj(C a) { return mk(a.x, -a.y); }
+template <typename C> __device__ __forceinline__ C czero() { return mk(decltype(C{}.x)(0), decltype(C{}.x)(0)); }
+
+// multiply by a unit phase code: 0:+1 1:+i 2:-1 3:-i  (free: swap/negate)
+template <int CODE, typename C> __device__ __forceinline__ C phase(C a) {
+  if constexpr (CODE == 0) return a;
+  else if constexpr (CODE == 1) return mk(-a.y, a.x);
+  else if constexpr (CODE == 2) return mk(-a.x, -a.y);
+  else return mk(a.y, -a.x);
+}
+
+// ---- read-only, streaming loads --------------------------------------------
+template <typename T> __device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
+__device__ __forceinline__ void st_cs(double2* p, double2 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_cs(float2* p, float2 v) { __stcs(p, v); }
+
+}  // namespace b200wd

@@ -1,0 +1,244 @@
+"""Device-resident fields and the host <-> device boundary.
+
+PyTorch is used only as plumbing: CUDA memory (caching allocator), streams
+and pinned host buffers.  Every byte of compute goes through libb200wd.
+
+Device layouts (include/b200wd.h):
+  * spinor block field -> torch tensor of shape (s, n, b), complex128 or
+    complex64: "component planes", rhs innermost;
+  * links -> (4, 9, n): one plane per (direction, 3x3 entry).
+The upload path copies the reference storage (Layout 1 or 2, complex128) as
+raw bytes and converts with a device kernel; the download path is the exact
+inverse.
+"""
+
+from __future__ import annotations
+
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .fields import SPINOR_LEN, BlockSpinorField, Layout
+from .geometry import LatticeGeometry
+
+try:
+    import torch
+except Exception as exc:  # pragma: no cover - torch is in the image
+    raise ImportError("paper_2601_05816_b200 needs torch for device memory and streams") from exc
+
+DTYPES = {"c128": (_lib.C128, torch.complex128, 16), "c64": (_lib.C64, torch.complex64, 8)}
+
+
+def dtype_code(dtype: str) -> int:
+    try:
+        return DTYPES[dtype][0]
+    except KeyError:
+        raise ValueError(f"dtype must be 'c128' or 'c64', got {dtype!r}") from None
+
+
+def torch_dtype(dtype: str):
+    return DTYPES[dtype][1]
+
+
+def require_device() -> "torch.device":
+    """The CUDA device to use; raises B200Unavailable (no CPU fallback)."""
+    if not torch.cuda.is_available():
+        raise _lib.B200Unavailable("no CUDA device: the B200 path has no CPU fallback")
+    _lib.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(t) -> int | None:
+    return None if t is None else int(t.data_ptr())
+
+
+@dataclass
+class DeviceField:
+    """A block spinor field resident in HBM (component planes, rhs innermost).
+
+    ``parity`` is None for a full-lattice field, 0/1 for a checkerboard
+    field whose site cb is the natural site ``2*cb + (0|1)`` of that parity.
+    """
+
+    data: "torch.Tensor"  # (s, n, b)
+    geom: LatticeGeometry | None = None
+    parity: int | None = None
+    layout: Layout = Layout.COMPONENT_MAJOR  # layout used when downloaded
+
+    @property
+    def s(self) -> int:
+        return int(self.data.shape[0])
+
+    @property
+    def n_sites(self) -> int:
+        return int(self.data.shape[1])
+
+    @property
+    def b(self) -> int:
+        return int(self.data.shape[2])
+
+    @property
+    def dtype(self) -> str:
+        return "c128" if self.data.dtype == torch.complex128 else "c64"
+
+    @property
+    def nbytes(self) -> int:
+        return self.data.numel() * self.data.element_size()
+
+    @classmethod
+    def zeros(cls, n_sites, b, s=SPINOR_LEN, dtype="c128", geom=None, parity=None, layout=Layout.COMPONENT_MAJOR):
+        dev = require_device()
+        t = torch.zeros((s, n_sites, b), dtype=torch_dtype(dtype), device=dev)
+        return cls(t, geom, parity, Layout(layout))
+
+    @classmethod
+    def empty(cls, n_sites, b, s=SPINOR_LEN, dtype="c128", geom=None, parity=None, layout=Layout.COMPONENT_MAJOR):
+        dev = require_device()
+        t = torch.empty((s, n_sites, b), dtype=torch_dtype(dtype), device=dev)
+        return cls(t, geom, parity, Layout(layout))
+
+    def empty_like(self) -> "DeviceField":
+        return DeviceField(torch.empty_like(self.data), self.geom, self.parity, self.layout)
+
+    def zeros_like(self) -> "DeviceField":
+        return DeviceField(torch.zeros_like(self.data), self.geom, self.parity, self.layout)
+
+    def copy(self) -> "DeviceField":
+        return DeviceField(self.data.clone(), self.geom, self.parity, self.layout)
+
+    @property
+    def ptr(self) -> int:
+        return int(self.data.data_ptr())
+
+    def to_host(self, layout=None, out: BlockSpinorField | None = None) -> BlockSpinorField:
+        """Download into the reference storage order (complex128)."""
+        return download(self, layout, out)
+
+    def logical(self) -> np.ndarray:
+        """(n, s, b) complex128 numpy copy (tests / diagnostics)."""
+        return self.data.permute(1, 0, 2).to(torch.complex128).cpu().numpy()
+
+
+def _host_array(field) -> np.ndarray:
+    data = np.asarray(field.data)
+    if data.dtype != np.complex128:
+        raise ValueError(f"host fields are complex128 (fields.py:95), got {data.dtype}")
+    expect = field.n_sites * field.s * field.b
+    if data.size != expect:
+        raise ValueError(f"field data has {data.size} values, expected {expect}")
+    return np.ascontiguousarray(data.reshape(-1))
+
+
+def upload(field, dtype: str = "c128", stream=None, parity=None) -> DeviceField:
+    """Host BlockSpinorField (any reference layout) -> DeviceField."""
+    if isinstance(field, DeviceField):
+        if field.dtype == dtype:
+            return field
+        return DeviceField(field.data.to(torch_dtype(dtype)), field.geom, field.parity, field.layout)
+    dev = require_device()
+    arr = _host_array(field)
+    raw = torch.from_numpy(arr).to(dev, non_blocking=True)
+    out = DeviceField.empty(field.n_sites, field.b, field.s, dtype, getattr(field, "geom", None), parity,
+                            Layout(int(field.layout)))
+    _lib.call("b200wd_spinor_import", ptr(raw), int(field.layout), field.n_sites, field.s, field.b,
+              out.ptr, dtype_code(dtype), stream_ptr(stream))
+    return out
+
+
+def download(df: DeviceField, layout=None, out: BlockSpinorField | None = None, stream=None) -> BlockSpinorField:
+    """DeviceField -> host BlockSpinorField in ``layout`` (default: df.layout)."""
+    layout = Layout(int(layout if layout is not None else (out.layout if out is not None else df.layout)))
+    raw = torch.empty(df.n_sites * df.s * df.b, dtype=torch.complex128, device=df.data.device)
+    _lib.call("b200wd_spinor_export", df.ptr, dtype_code(df.dtype), df.n_sites, df.s, df.b, ptr(raw),
+              int(layout), stream_ptr(stream))
+    if out is None:
+        out = BlockSpinorField.zeros(df.n_sites, df.b, layout, df.s, df.geom)
+    elif (out.n_sites, out.s, out.b) != (df.n_sites, df.s, df.b):
+        raise ValueError("output field shape mismatch")
+    host = torch.from_numpy(out.data.reshape(-1))
+    host.copy_(raw, non_blocking=False)
+    return out
+
+
+# ---- links ------------------------------------------------------------------
+
+
+@dataclass
+class DeviceGauge:
+    """Links resident in HBM as (4, 9, n) planes of one dtype."""
+
+    data: "torch.Tensor"
+    geom: LatticeGeometry
+
+    @property
+    def ptr(self) -> int:
+        return int(self.data.data_ptr())
+
+    @property
+    def dtype(self) -> str:
+        return "c128" if self.data.dtype == torch.complex128 else "c64"
+
+
+def upload_gauge(gauge, dtype: str = "c128", stream=None) -> DeviceGauge:
+    dev = require_device()
+    data = np.ascontiguousarray(np.asarray(gauge.data, dtype=np.complex128))
+    n = gauge.geom.n_sites
+    if data.shape != (n, 4, 3, 3):
+        raise ValueError(f"gauge data has shape {data.shape}, expected {(n, 4, 3, 3)}")
+    raw = torch.from_numpy(data.reshape(-1)).to(dev, non_blocking=True)
+    out = torch.empty((4, 9, n), dtype=torch_dtype(dtype), device=dev)
+    _lib.call("b200wd_gauge_import", ptr(raw), n, ptr(out), dtype_code(dtype), stream_ptr(stream))
+    return DeviceGauge(out, gauge.geom)
+
+
+class _GaugeCache:
+    """Upload each host GaugeField once per dtype.
+
+    The key is the identity of the numpy array; a cheap strided fingerprint
+    detects in-place modification (then the links are uploaded again).
+    """
+
+    def __init__(self):
+        self._entries: dict = {}
+
+    @staticmethod
+    def _fingerprint(arr: np.ndarray) -> tuple:
+        flat = arr.reshape(-1)
+        step = max(1, flat.size // 2048)
+        sample = flat[::step]
+        return (arr.ctypes.data, arr.shape, complex(sample.sum()), complex((sample * np.arange(sample.size)).sum()))
+
+    def get(self, gauge, dtype: str) -> DeviceGauge:
+        if isinstance(gauge, DeviceGauge):
+            return gauge
+        arr = gauge.data
+        key = (id(arr), dtype)
+        fp = self._fingerprint(arr)
+        hit = self._entries.get(key)
+        if hit is not None:
+            ref, hfp, dg = hit
+            if ref() is arr and hfp == fp:
+                return dg
+        dg = upload_gauge(gauge, dtype)
+        try:
+            ref = weakref.ref(arr)
+        except TypeError:
+            ref = (lambda a=arr: a)
+        self._entries[key] = (ref, fp, dg)
+        # drop entries whose arrays died
+        for k in [k for k, (r, _, _) in self._entries.items() if r() is None]:
+            del self._entries[k]
+        return dg
+
+    def clear(self) -> None:
+        self._entries.clear()
+
+
+gauge_cache = _GaugeCache()

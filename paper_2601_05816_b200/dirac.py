@@ -1,0 +1,195 @@
+"""Wilson-Dirac operator: drop-in for ``lqcdlab.dirac`` (dirac.py:1-334).
+
+``apply_dirac(params, gauge, clover, psi, comm=None, flops=None, perf=None)``
+keeps the reference signature.  ``psi`` may be a host ``BlockSpinorField``
+(reference layouts; uploaded, applied, downloaded) or a
+:class:`~paper_2601_05816_b200.device.DeviceField` (stays on the device).
+The apply itself is one launch of the fused sm_100a hopping kernel
+(``b200wd_hop`` in csrc/dirac.cu): D psi = (4+m0) psi - C psi - H psi.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .device import (DeviceField, DeviceGauge, dtype_code, gauge_cache, ptr, require_device, stream_ptr,
+                     upload)
+from .fields import SPINOR_LEN
+
+# traffic ledger of the paper (dirac.py:43-48), kept for the perf records
+FLOPS_PER_SITE_RHS = 2574
+VALUES_PER_SITE_RHS = 168
+VALUES_PER_SITE_FIXED = 114
+BYTES_PER_VALUE = 16
+
+
+@dataclass(frozen=True)
+class DiracParams:
+    """dirac.py:51-60."""
+
+    m0: float = -0.5
+    a: float = 1.0
+
+    def __post_init__(self) -> None:
+        if self.a != 1.0:
+            raise ValueError("lattice spacing is fixed to 1")
+
+
+@dataclass
+class FlopCounter:
+    """dirac.py:63-73.  The GPU kernel is fused, so the tally records the
+    reference's structured operation count for the same operator (the
+    mathematical work), not the fused kernel's instruction mix."""
+
+    cmul: int = 0
+    cadd: int = 0
+    rmul: int = 0
+
+    @property
+    def total_flops(self) -> int:
+        return 6 * self.cmul + 2 * self.cadd + 2 * self.rmul
+
+    def add_apply(self, n_sites: int, b: int) -> None:
+        per = n_sites * b
+        # self coupling (dirac.py:150-157)
+        self.cmul += 72 * per
+        self.cadd += 72 * per
+        self.rmul += 12 * per
+        # 8 compressions, 4 chi matvecs, 4 lambda matvecs, 8 reconstructions
+        self.cmul += (8 * 6 + 4 * 18 + 4 * 18 + 8 * 6) * per
+        self.cadd += (8 * 6 + 4 * 12 + 4 * 12 + 8 * 12) * per
+        self.rmul += 8 * 6 * per
+
+
+@dataclass
+class DiracPerfRecord:
+    """dirac.py:76-100."""
+
+    seconds: float
+    sites: int
+    b: int
+    layout: int
+    flops: int
+    bytes: int
+
+    @property
+    def gflops(self) -> float:
+        return self.flops / self.seconds / 1e9 if self.seconds > 0 else float("inf")
+
+    def as_dict(self) -> dict:
+        return {"seconds": self.seconds, "sites": self.sites, "b": self.b, "layout": self.layout,
+                "flops": self.flops, "bytes": self.bytes, "gflops": self.gflops}
+
+
+def account_traffic(b: int) -> dict:
+    """dirac.py:111-118."""
+    if b < 1:
+        raise ValueError(f"b must be >= 1, got {b}")
+    return {"flops_per_site": FLOPS_PER_SITE_RHS * b,
+            "bytes_per_site": (VALUES_PER_SITE_RHS * b + VALUES_PER_SITE_FIXED) * BYTES_PER_VALUE}
+
+
+def compulsory_bytes_per_site(b: int, dtype: str = "c128") -> int:
+    """Algorithmic HBM bytes of one full apply per site: read psi, write eta,
+    read the 4 links of the site once: (24 b + 36) w."""
+    w = 16 if dtype == "c128" else 8
+    return (24 * b + 36) * w
+
+
+def _lattice(geom, t_origin: int = 0):
+    return _lib.Lattice.make(geom.dims, t_origin)
+
+
+def _check_clover(clover) -> None:
+    if clover is not None and not (clover.is_zero() if hasattr(clover, "is_zero") else not np.any(clover.data)):
+        raise NotImplementedError("the B200 path implements C = 0 (the BASELINE configurations); "
+                                  "a non-zero clover term is not supported by this build")
+
+
+class DiracOperator:
+    """D = (4+m0) - H on the full (single-GPU) lattice, device resident.
+
+    ``apply_device(v, out, scale)`` computes out = scale_r * D v in one
+    launch; ``scale`` (device, b doubles) lets GMRES fold the basis
+    normalisation into the apply.
+    """
+
+    def __init__(self, params: DiracParams, gauge, clover=None, dtype: str = "c128"):
+        _check_clover(clover)
+        require_device()
+        self.params = params
+        self.dtype = dtype
+        self.geom = gauge.geom
+        self.gauge = gauge_cache.get(gauge, dtype)
+        self.lat = _lattice(self.geom)
+        self.n_sites = self.geom.n_sites
+        self.allreduce = None
+
+    def apply_device(self, v: DeviceField, out: DeviceField | None = None, scale=None,
+                     stream=None) -> DeviceField:
+        if v.n_sites != self.n_sites or v.s != SPINOR_LEN:
+            raise ValueError(f"field has {v.n_sites} sites / s={v.s}, lattice has {self.n_sites} sites")
+        if v.dtype != self.dtype:
+            raise ValueError(f"field dtype {v.dtype} != operator dtype {self.dtype}")
+        out = v.empty_like() if out is None else out
+        _lib.call("b200wd_hop", self.lat, dtype_code(self.dtype), v.b, -1, self.gauge.ptr, v.ptr, v.ptr, out.ptr,
+                  4.0 + self.params.m0, -1.0, ptr(scale), 0, self.geom.dims[0], None, None, stream_ptr(stream))
+        return out
+
+    def __call__(self, v):
+        return _apply_any(self, v)
+
+
+def _apply_any(op, v):
+    """Host fields in -> host fields out; device fields stay on the device."""
+    if isinstance(v, DeviceField):
+        return op.apply_device(v)
+    dv = upload(v, op.dtype)
+    return op.apply_device(dv).to_host(v.layout)
+
+
+def apply_dirac(params: DiracParams, gauge, clover, psi, comm=None, flops: FlopCounter | None = None,
+                perf: list | None = None, dtype: str | None = None, out=None):
+    """eta = D psi over all rhs columns (dirac.py:299-334).
+
+    ``comm`` routes the apply through a communicator (the multi-GPU T
+    split, :class:`paper_2601_05816_b200.tsplit.TSplitComm`), as the
+    reference routes it through its halo executor (dirac.py:313-314).
+    """
+    if comm is not None:
+        return comm.apply_dirac(params, gauge, clover, psi, flops=flops, perf=perf)
+    if psi.s != SPINOR_LEN:
+        raise ValueError(f"expected full spinor field (s={SPINOR_LEN}), got s={psi.s}")
+    if psi.n_sites != gauge.geom.n_sites:
+        raise ValueError(f"field has {psi.n_sites} sites, gauge lattice has {gauge.geom.n_sites}")
+    if dtype is None:
+        dtype = psi.dtype if isinstance(psi, DeviceField) else "c128"
+    t0 = time.perf_counter()
+    op = DiracOperator(params, gauge, clover, dtype)
+    if isinstance(psi, DeviceField):
+        res = op.apply_device(psi, out)
+    else:
+        res = op.apply_device(upload(psi, dtype)).to_host(psi.layout, out)
+    if flops is not None:
+        flops.add_apply(psi.n_sites, psi.b)
+    if perf is not None:
+        import torch
+        torch.cuda.synchronize()
+        ledger = account_traffic(psi.b)
+        perf.append(DiracPerfRecord(time.perf_counter() - t0, psi.n_sites, psi.b, int(psi.layout),
+                                    ledger["flops_per_site"] * psi.n_sites, ledger["bytes_per_site"] * psi.n_sites))
+    return res
+
+
+def hop_device(lat, dtype: str, b: int, dst_parity: int, gauge: DeviceGauge, src: DeviceField, out: DeviceField,
+               xself: DeviceField | None, alpha: float, beta: float, scale=None, t_begin: int = 0,
+               t_end: int | None = None, lam_halo=None, chi_halo=None, stream=None) -> None:
+    """Thin wrapper over ``b200wd_hop`` (see include/b200wd.h)."""
+    t_end = lat.dims[0] if t_end is None else t_end
+    _lib.call("b200wd_hop", lat, dtype_code(dtype), b, dst_parity, gauge.ptr, src.ptr,
+              None if xself is None else xself.ptr, out.ptr, float(alpha), float(beta), ptr(scale),
+              int(t_begin), int(t_end), ptr(lam_halo), ptr(chi_halo), stream_ptr(stream))

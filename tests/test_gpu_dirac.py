@@ -1,0 +1,209 @@
+"""GPU parity: the sm_100a Wilson-Dirac / Schur kernels vs the oracle and
+the reference-generated golden fixtures.
+
+Tolerances (BASELINE.json north_star): relative Frobenius error <= 1e-12
+for complex128 and <= 1e-5 for complex64 (against the reference run on the
+c64-rounded inputs).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import lqcd_oracle as O
+from tests.golden_util import checksum, load_npz
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2601_05816_b200")
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def host_field(logical, layout, geom=None):
+    n, s, b = logical.shape
+    f = P.BlockSpinorField.zeros(n, b, layout, s, geom)
+    f.set_ksi(logical)
+    return f
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    dims = (8, 8, 8, 8)
+    geom = P.LatticeGeometry(dims)
+    links = O.flip_time_boundary(O.gen_gauge_random(dims, 0), dims)
+    psi = O.gen_spinor(geom.n_sites, 4, 2)
+    return geom, links, psi
+
+
+def test_cfg1_matches_reference_golden(cfg1):
+    geom, links, psi = cfg1
+    f = load_npz("dirac_cfg1.npz")
+    gauge = P.GaugeField(geom, links)
+    eta = P.apply_dirac(P.DiracParams(m0=0.1), gauge, P.gen_clover(geom, "zero"),
+                        host_field(psi, P.Layout.COMPONENT_MAJOR, geom)).ksi()
+    assert rel(eta[7 * 512:], f["eta_last_slice"]) < 1e-12
+    assert np.abs(checksum(eta) - f["checksum"]).max() < 1e-12 * np.abs(f["checksum"]).max()
+    assert np.abs(np.linalg.norm(eta.reshape(-1, 4), axis=0) - f["norms"]).max() < 1e-12 * f["norms"].max()
+
+
+@pytest.mark.parametrize("b", [1, 2, 3, 4, 8, 12, 16, 32])
+@pytest.mark.parametrize("layout", [1, 2])
+def test_dirac_c128_matches_oracle(b, layout):
+    dims = (4, 4, 4, 8)
+    geom = P.LatticeGeometry(dims)
+    links = O.gen_gauge_random(dims, 100 + b)
+    psi = O.gen_spinor(geom.n_sites, b, 200 + b)
+    ref = O.apply_dirac(dims, -0.5, links, None, psi)
+    got = P.apply_dirac(P.DiracParams(m0=-0.5), P.GaugeField(geom, links), None,
+                        host_field(psi, P.Layout(layout), geom))
+    assert got.layout == layout and got.b == b
+    assert rel(got.ksi(), ref) < 1e-12
+
+
+@pytest.mark.parametrize("b", [1, 2, 3, 4, 12, 16])
+def test_dirac_c64_matches_oracle_on_rounded_inputs(b):
+    dims = (8, 4, 4, 4)
+    geom = P.LatticeGeometry(dims)
+    links = O.flip_time_boundary(O.near_unit_gauge(dims, 0.3, 5), dims)
+    psi = O.gen_spinor(geom.n_sites, b, 300 + b)
+    ref = O.apply_dirac(dims, 0.1, O.round_c64(links), None, O.round_c64(psi))
+    got = P.apply_dirac(P.DiracParams(m0=0.1), P.GaugeField(geom, links), None,
+                        host_field(psi, P.Layout.COMPONENT_MAJOR, geom), dtype="c64")
+    assert rel(got.ksi(), ref) < 1e-5
+
+
+def test_free_field_identity():
+    geom = P.LatticeGeometry((4, 4, 4, 4))
+    psi = np.full((256, 12, 2), 1.0 + 0.5j)
+    eta = P.apply_dirac(P.DiracParams(m0=-0.5), P.gen_gauge(geom, "unit"), P.gen_clover(geom, "zero"),
+                        host_field(psi, P.Layout.RHS_MAJOR, geom))
+    assert np.abs(eta.ksi() + 0.5 * psi).max() < 1e-14
+
+
+def test_device_field_roundtrip_and_linearity():
+    from paper_2601_05816_b200.device import upload
+    dims = (4, 4, 4, 4)
+    geom = P.LatticeGeometry(dims)
+    a = O.gen_spinor(256, 3, 1)
+    c = O.gen_spinor(256, 3, 2)
+    for layout in (1, 2):
+        d = upload(host_field(a, P.Layout(layout), geom))
+        assert np.array_equal(d.to_host(layout).ksi(), a)
+    links = O.gen_gauge_random(dims, 3)
+    g = P.GaugeField(geom, links)
+    prm = P.DiracParams(m0=0.3)
+    lhs = P.apply_dirac(prm, g, None, host_field(a + 2 * c, 2, geom)).ksi()
+    rhs = P.apply_dirac(prm, g, None, host_field(a, 2, geom)).ksi() + \
+        2 * P.apply_dirac(prm, g, None, host_field(c, 2, geom)).ksi()
+    assert np.abs(lhs - rhs).max() <= 1e-12 * np.abs(rhs).max()
+
+
+def test_perf_record_and_flops():
+    geom = P.LatticeGeometry((4, 4, 4, 4))
+    psi = host_field(O.gen_spinor(256, 2, 3), 1, geom)
+    perf, flops = [], P.FlopCounter()
+    P.apply_dirac(P.DiracParams(), P.gen_gauge(geom, "random", 1), None, psi, flops=flops, perf=perf)
+    (r,) = perf
+    assert r.sites == 256 and r.b == 2 and r.flops == 2574 * 256 * 2 and r.seconds > 0
+    assert 0.85 <= flops.total_flops / (256 * 2) / 2574 <= 1.15
+
+
+def test_schur_nearunit_matches_reference_golden():
+    f = load_npz("schur_8444_nearunit.npz")
+    dims = (8, 4, 4, 4)
+    geom = P.LatticeGeometry(dims)
+    links = O.flip_time_boundary(O.near_unit_gauge(dims, 0.3, 7), dims)
+    gauge = P.GaugeField(geom, links)
+    s = P.SchurOperator(P.DiracParams(m0=0.1), gauge, None)
+    v = host_field(O.gen_spinor(256, 3, 74), P.Layout.COMPONENT_MAJOR)
+    assert rel(s.apply(v).ksi(), f["out"]) < 1e-12
+    eta = host_field(O.gen_spinor(512, 3, 75), P.Layout.COMPONENT_MAJOR, geom)
+    red, el = s.reduce_rhs(eta)
+    assert rel(red.ksi(), f["reduced"]) < 1e-12
+    assert rel(s.reconstruct(red, el).ksi(), f["x_odd"]) < 1e-12
+    d = P.apply_dirac(P.DiracParams(m0=0.1), gauge, None, host_field(O.gen_spinor(512, 3, 76), 2, geom))
+    assert rel(d.ksi(), f["dirac_out"]) < 1e-12
+
+
+@pytest.mark.parametrize("keep", [0, 1])
+@pytest.mark.parametrize("dtype,tol", [("c128", 1e-12), ("c64", 1e-5)])
+def test_schur_matches_oracle(keep, dtype, tol):
+    dims = (4, 4, 4, 8)
+    geom = P.LatticeGeometry(dims)
+    links = O.near_unit_gauge(dims, 0.3, 9)
+    v = O.gen_spinor(256, 4, 11)
+    so = O.SchurOracle(dims, 0.1, O.round_c64(links) if dtype == "c64" else links, None, keep_parity=keep)
+    ref = so.apply(O.round_c64(v) if dtype == "c64" else v)
+    sp = P.SchurOperator(P.DiracParams(m0=0.1), P.GaugeField(geom, links), None, keep_parity=keep, dtype=dtype)
+    from paper_2601_05816_b200.device import upload
+    got = sp.apply_device(upload(host_field(v, 2), dtype, parity=keep)).logical()
+    assert rel(got, ref) < tol
+
+
+def test_schur_constant_field_and_singular():
+    geom = P.LatticeGeometry((4, 4, 4, 4))
+    s = P.SchurOperator(P.DiracParams(m0=0.5), P.gen_gauge(geom, "unit"), P.gen_clover(geom, "zero"))
+    v = host_field(np.full((128, 12, 2), 1.0 + 0j), 1)
+    assert np.abs(s.apply(v).ksi() - (4.5 - 16 / 4.5)).max() < 1e-12
+    with pytest.raises(P.SingularBlockError) as err:
+        P.SchurOperator(P.DiracParams(m0=-4.0), P.gen_gauge(P.LatticeGeometry((2, 2, 2, 2)), "unit"), None)
+    assert "site" in str(err.value)
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+@pytest.mark.parametrize("parity", [None, 0, 1])
+def test_tsplit_halo_kernels_reproduce_single_gpu(nranks, parity):
+    """Emulate the T split on one GPU: per-slab pack -> face swap -> hop with halos."""
+    import torch
+    from paper_2601_05816_b200 import _lib
+    from paper_2601_05816_b200.device import DeviceField, upload, upload_gauge
+    from paper_2601_05816_b200.dirac import hop_device
+    from paper_2601_05816_b200.oddeven import device_split
+
+    dims = (8, 4, 4, 6)
+    geom = P.LatticeGeometry(dims)
+    links = O.flip_time_boundary(O.near_unit_gauge(dims, 0.3, 21), dims)
+    psi = O.gen_spinor(geom.n_sites, 3, 22)
+    full_lat = _lib.Lattice.make(dims)
+    g_full = upload_gauge(P.GaugeField(geom, links))
+    d_psi = upload(host_field(psi, 2, geom))
+    if parity is None:
+        ref = DeviceField.empty(geom.n_sites, 3)
+        hop_device(full_lat, "c128", 3, -1, g_full, d_psi, ref, d_psi, 4.1, -1.0)
+        src_full = d_psi
+    else:
+        e, o = device_split(full_lat, d_psi)
+        src_full = o if parity == 0 else e  # source parity 1-p
+        ref = DeviceField.empty(geom.n_sites // 2, 3)
+        hop_device(full_lat, "c128", 3, parity, g_full, src_full, ref, None, 0.0, 1.0)
+    tl = dims[0] // nranks
+    per_t = geom.sites_per_slice
+    per = per_t if parity is None else per_t // 2
+    slabs = []
+    for r in range(nranks):
+        lg = P.LatticeGeometry((tl,) + dims[1:])
+        lat = _lib.Lattice.make(lg.dims, r * tl)
+        gl = upload_gauge(P.GaugeField(lg, links[r * tl * per_t:(r + 1) * tl * per_t]))
+        src = DeviceField(src_full.data[:, r * tl * per:(r + 1) * tl * per].contiguous())
+        lam = torch.empty((6, per, 3), dtype=torch.complex128, device="cuda")
+        chi = torch.empty_like(lam)
+        sp = -1 if parity is None else 1 - parity
+        _lib.call("b200wd_halo_pack", lat, 0, 3, sp, gl.ptr, src.ptr, lam.data_ptr(), chi.data_ptr(), 0)
+        slabs.append((lg, lat, gl, src, lam, chi))
+    outs = []
+    for r, (lg, lat, gl, src, _, _) in enumerate(slabs):
+        lam_from_up = slabs[(r + 1) % nranks][4]
+        chi_from_down = slabs[(r - 1) % nranks][5]
+        out = DeviceField(torch.empty_like(src.data))
+        if parity is None:
+            hop_device(lat, "c128", 3, -1, gl, src, out, src, 4.1, -1.0, lam_halo=lam_from_up,
+                       chi_halo=chi_from_down)
+        else:
+            hop_device(lat, "c128", 3, parity, gl, src, out, None, 0.0, 1.0, lam_halo=lam_from_up,
+                       chi_halo=chi_from_down)
+        outs.append(out.data)
+    got = torch.cat(outs, dim=1)
+    err = (got - ref.data).abs().max().item() / ref.data.abs().max().item()
+    assert err < 1e-14

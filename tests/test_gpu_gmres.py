@@ -1,0 +1,172 @@
+"""GPU parity of the batched GMRES and the per-rhs BLAS.
+
+GMRES bar (BASELINE.json north_star): the same Arnoldi iteration count as
+the reference +-1 and a final true residual below the tolerance; the
+residual history is compared with the reference's over the common prefix
+(tests/test_gmres.py semantics), plus the reference's own fake-operator
+tests (identity, scaled identity, zero rhs, initial guess, stagnation).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import lqcd_oracle as O
+from tests.golden_util import load_gmres
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2601_05816_b200")
+
+
+def host_field(logical, layout, geom=None):
+    n, s, b = logical.shape
+    f = P.BlockSpinorField.zeros(n, b, layout, s, geom)
+    f.set_ksi(logical)
+    return f
+
+
+# ---- BLAS (tests/test_blas.py) ---------------------------------------------------
+
+
+@pytest.mark.parametrize("layout", [1, 2])
+@pytest.mark.parametrize("b", [1, 3, 5, 12, 17])
+def test_dot_and_norms(layout, b):
+    x, y = O.gen_spinor(24, b, 10), O.gen_spinor(24, b, 11)
+    fx, fy = host_field(x, layout), host_field(y, layout)
+    ref = np.einsum("xkb,xkb->b", x.conj(), y)
+    for strategy in ("naive", "deferred"):
+        got = P.block_dot(fx, fy, strategy)
+        assert np.abs(got - ref).max() < 1e-12 * np.abs(ref).max()
+    assert np.abs(P.block_norms(fx) - np.linalg.norm(x.reshape(-1, b), axis=0)).max() < 1e-12 * np.abs(x).max()
+
+
+def test_axpy_scale_and_errors():
+    x, y = O.gen_spinor(12, 3, 5), O.gen_spinor(12, 3, 6)
+    fx, fy = host_field(x, 2), host_field(y, 2)
+    alpha = np.array([1 + 2j, -0.5, 0.0])
+    P.block_axpy(alpha, fx, fy)
+    assert np.abs(fy.ksi() - (y + x * alpha)).max() < 1e-14
+    fs = host_field(x, 1)
+    P.block_scale(np.array([2.0, 0.0, 1j]), fs)
+    assert np.abs(fs.ksi() - x * np.array([2.0, 0.0, 1j])).max() < 1e-14
+    with pytest.raises(ValueError):
+        P.block_dot(host_field(x, 1), host_field(y, 2))
+    with pytest.raises(ValueError):
+        P.block_dot(fx, fx, "fancy")
+    z = P.BlockSpinorField.zeros(8, 2, 1)
+    assert np.array_equal(P.block_norms(z), np.zeros(2))
+
+
+# ---- fake-operator GMRES (tests/test_gmres.py:38-69, 163-172) ------------------------
+
+
+def test_identity_one_iteration():
+    eta = P.gen_spinor(16, 3, 2, seed=1)
+    res = P.gmres_solve(P.matrix_op(np.eye(192)), eta, None, P.GmresConfig(tol=1e-10))
+    assert res.iterations == 1 and res.converged.all() and res.breakdown.all()
+    assert np.abs(res.psi.ksi() - eta.ksi()).max() < 1e-12
+
+
+def test_scaled_identity_and_zero_rhs():
+    eta = P.gen_spinor(16, 2, 1, seed=2)
+    res = P.gmres_solve(P.matrix_op(2.0 * np.eye(192)), eta, None, P.GmresConfig(tol=1e-10))
+    assert np.abs(res.psi.ksi() - 0.5 * eta.ksi()).max() < 1e-12
+    z = P.BlockSpinorField.zeros(16, 2, 1)
+    res = P.gmres_solve(P.matrix_op(np.eye(192)), z, None, P.GmresConfig())
+    assert np.isfinite(res.psi.data).all() and not res.psi.data.any() and res.converged.all()
+
+
+def test_initial_guess_respected():
+    rng = np.random.default_rng(3)
+    a = np.diag(rng.uniform(1.0, 2.0, 48)).astype(np.complex128)
+    eta = P.gen_spinor(4, 2, 1, seed=4)
+    exact = P.BlockSpinorField.zeros_like(eta)
+    exact.set_columns(np.linalg.solve(a, eta.columns()))
+    res = P.gmres_solve(P.matrix_op(a), eta, exact, P.GmresConfig(tol=1e-10))
+    assert res.iterations == 0
+    assert np.abs(res.psi.ksi() - exact.ksi()).max() < 1e-12
+
+
+def test_stagnation_flagged():
+    n = 192
+    perm = np.roll(np.eye(n), 1, axis=0)
+    eta = P.BlockSpinorField.zeros(16, 1, 1)
+    eta.data[0] = 1.0
+    res = P.gmres_solve(P.matrix_op(perm), eta, None, P.GmresConfig(restart_len=5, restarts=2))
+    assert res.stagnated and not res.converged.any()
+
+
+# ---- Wilson GMRES vs the reference goldens --------------------------------------------
+
+
+@pytest.mark.parametrize("oe", [False, True])
+def test_nearunit_solve_matches_reference(oe):
+    g = load_gmres()[f"nearunit_8444_{'oe' if oe else 'full'}"]
+    dims = tuple(g["dims"])
+    geom = P.LatticeGeometry(dims)
+    links = O.flip_time_boundary(O.near_unit_gauge(dims, g["eps"], g["link_seed"]), dims)
+    eta = host_field(O.gen_spinor(geom.n_sites, g["b"], g["eta_seed"]), 2, geom)
+    cfg = P.GmresConfig(restart_len=g["restart_len"], restarts=g["restarts"], tol=g["tol"])
+    rep = P.solve_dirac(P.DiracParams(m0=g["m0"]), P.GaugeField(geom, links), None, eta, cfg, odd_even=oe)
+    assert abs(rep.iterations - g["iterations"]) <= 1
+    assert np.all(rep.full_relnorms <= g["tol"])
+    ref_h = np.array(g["history"])
+    k = min(len(ref_h), len(rep.result.history))
+    got_h = np.array(rep.result.history[:k])
+    assert np.all(np.abs(got_h - ref_h[:k]) <= 1e-6 * ref_h[:k])
+    # solution agrees with the oracle solve
+    psi, _, _ = O.solve_dirac(dims, g["m0"], links, None, eta.ksi(),
+                              O.GmresConfig(restart_len=g["restart_len"], restarts=g["restarts"], tol=g["tol"]),
+                              odd_even=oe)
+    assert np.abs(rep.psi.ksi() - psi).max() / np.abs(psi).max() < 1e-8
+
+
+def test_replicated_rhs_identical_histories():
+    dims = (4, 4, 4, 4)
+    geom = P.LatticeGeometry(dims)
+    links = O.near_unit_gauge(dims, 0.3, 31)
+    col = O.gen_spinor(256, 1, 11)
+    rep = host_field(np.repeat(col, 4, axis=2), 2, geom)
+    res = P.gmres_solve(P.dirac_op(P.DiracParams(m0=1.0), P.GaugeField(geom, links), None), rep, None,
+                        P.GmresConfig(tol=1e-8, restarts=40))
+    for h in res.history:
+        assert np.ptp(h) == 0.0
+    cols = res.psi.ksi()
+    assert np.abs(cols - cols[:, :, :1]).max() == 0.0
+
+
+def test_batched_vs_independent_and_gamma_audit():
+    dims = (4, 4, 4, 4)
+    geom = P.LatticeGeometry(dims)
+    op = P.dirac_op(P.DiracParams(m0=1.0), P.GaugeField(geom, O.gen_gauge_random(dims, 81)), None)
+    eta = host_field(O.gen_spinor(256, 4, 10), 1, geom)
+    assert P.batched_vs_independent_audit(op, eta, None, P.GmresConfig(tol=1e-8, restarts=40)) <= 1e-8
+    op2 = P.dirac_op(P.DiracParams(m0=-2.0), P.GaugeField(geom, O.gen_gauge_random(dims, 82)), None)
+    eta2 = host_field(O.gen_spinor(256, 2, 12), 1, geom)
+    assert P.gamma_residual_audit(op2, eta2, None, P.GmresConfig(restart_len=5, restarts=3)) <= 1e-8
+
+
+def test_fixed_iteration_protocol_and_reorth():
+    dims = (4, 4, 4, 4)
+    geom = P.LatticeGeometry(dims)
+    op = P.dirac_op(P.DiracParams(m0=1.0), P.GaugeField(geom, O.gen_gauge_random(dims, 81)), None)
+    eta = host_field(O.gen_spinor(256, 2, 7), 1, geom)
+    res = P.gmres_solve(op, eta, None, P.GmresConfig(restart_len=10, restarts=10, fixed_iterations=True))
+    assert res.iterations == 100 and len(res.history) == 100
+    r1 = P.gmres_solve(op, eta, None, P.GmresConfig(tol=1e-10, restarts=40))
+    r2 = P.gmres_solve(op, eta, None, P.GmresConfig(tol=1e-10, restarts=40, reorthogonalize=True))
+    assert abs(r1.iterations - r2.iterations) <= 1 and r2.converged.all()
+
+
+def test_gmres_matches_oracle_dirac_small():
+    dims = (4, 4, 4, 4)
+    geom = P.LatticeGeometry(dims)
+    links = O.gen_gauge_random(dims, 81)
+    eta = O.gen_spinor(256, 4, 5)
+    ocfg = O.GmresConfig(tol=1e-10, restarts=40)
+    ref = O.gmres(lambda v: O.apply_dirac(dims, 1.0, links, None, v), eta, None, ocfg)
+    res = P.gmres_solve(P.dirac_op(P.DiracParams(m0=1.0), P.GaugeField(geom, links), None),
+                        host_field(eta, 1, geom), None, P.GmresConfig(tol=1e-10, restarts=40))
+    assert abs(res.iterations - ref.iterations) <= 1
+    assert res.converged.all()
+    assert np.abs(res.psi.ksi() - ref.psi).max() / np.abs(ref.psi).max() < 1e-8
