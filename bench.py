@@ -114,10 +114,10 @@ def gpu_sweep(args, torch, P):
             field_bytes = n * 12 * b * w
             nbuf = max(2, int(np.ceil(4 * l2 / (2 * field_bytes))) + 1)
             g = torch.Generator(device="cpu").manual_seed(b)
-            base = torch.randn((12, n, b), dtype=torch.complex128, generator=g)
+            base = torch.randn((n // 8, 12, 8, b), dtype=torch.complex128, generator=g)
             tdt = torch.complex128 if dt == "c128" else torch.complex64
-            psis = [DeviceField(base.to(dev, tdt)) for _ in range(nbuf)]
-            etas = [DeviceField(torch.empty_like(psis[0].data)) for _ in range(nbuf)]
+            psis = [DeviceField(base.to(dev, tdt), n) for _ in range(nbuf)]
+            etas = [DeviceField(torch.empty_like(psis[0].data), n) for _ in range(nbuf)]
             code = 0 if dt == "c128" else 1
 
             def launch(i):

@@ -38,33 +38,36 @@ def needs_build() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: Path | None = None) -> Path:
+    lib = Path(out) if out else LIB
+    if not force and out is None and not needs_build():
         return LIB
     objs = []
-    tmp = PKG / "build"
-    tmp.mkdir(exist_ok=True)
+    tmp = PKG / "build" / ("_".join(defines) or "default")
+    tmp.mkdir(parents=True, exist_ok=True)
     logs = []
     for src in SOURCES:
         obj = tmp / (Path(src).stem + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-I", str(CSRC), "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(ROOT / "include"), "-I", str(CSRC),
+               "-c", str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
         objs.append(str(obj))
     cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC",
-           *objs, "-o", str(LIB) + ".tmp"]
+           *objs, "-o", str(lib) + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{r.stderr}")
-    os.replace(str(LIB) + ".tmp", LIB)
+    os.replace(str(lib) + ".tmp", lib)
     (tmp / "ptxas.log").write_text("\n".join(logs))
     if verbose:
         print("\n".join(logs))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))
+    outs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose=True, defines=defs, out=Path(outs[0]) if outs else None))

@@ -11,7 +11,9 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libb200wd.so"
+import os
+
+LIB_PATH = Path(os.environ.get("B200WD_LIB") or Path(__file__).resolve().parent / "libb200wd.so")
 
 OK, ERR_ARG, ERR_CUDA, ERR_SINGULAR, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 C128, C64 = 0, 1

@@ -20,9 +20,13 @@ namespace b200wd {
 constexpr int kMaxGrid = 148 * 4;
 constexpr int kBlock = 256;
 
+// (site, component) groups of a field, storage padded to whole 8-site blocks
+__host__ __device__ __forceinline__ int64_t groups(int64_t n, int s) { return ((n + 7) / 8) * 8 * s; }
+
 static inline int rows_per_block(int b) { return b >= kBlock ? 1 : kBlock / b; }
 
 static inline int grid_for_sites(int64_t n, int S) {
+  n = ((n + 7) / 8) * 8 * 12;  // group count of a full spinor field (upper bound for s <= 12)
   int64_t g = (n + S - 1) / S;
   if (g > kMaxGrid) g = kMaxGrid;
   return (int)(g < 1 ? 1 : g);
@@ -97,10 +101,9 @@ __global__ void dot_kernel(int64_t n, int s, const double2* __restrict__ x, cons
                            double2* out, Scratch sc) {
   const int b = blockDim.x, r = threadIdx.x;
   double2 a = make_double2(0.0, 0.0);
-  for (int64_t site = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; site < n;
-       site += (int64_t)gridDim.x * blockDim.y)
-    for (int k = 0; k < s; ++k) {
-      const int64_t i = ((int64_t)k * n + site) * b + r;
+  const int64_t ng = groups(n, s);
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; g < ng; g += (int64_t)gridDim.x * blockDim.y) {
+      const int64_t i = g * b + r;
       acc_dot(a, __ldg(x + i), __ldg(yv + i));
     }
   reduce_finish(a, sc, out);
@@ -109,10 +112,9 @@ __global__ void dot_kernel(int64_t n, int s, const double2* __restrict__ x, cons
 __global__ void norm2_kernel(int64_t n, int s, const double2* __restrict__ x, double2* out, Scratch sc) {
   const int b = blockDim.x, r = threadIdx.x;
   double2 a = make_double2(0.0, 0.0);
-  for (int64_t site = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; site < n;
-       site += (int64_t)gridDim.x * blockDim.y)
-    for (int k = 0; k < s; ++k) {
-      const double2 v = __ldg(x + ((int64_t)k * n + site) * b + r);
+  const int64_t ng = groups(n, s);
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; g < ng; g += (int64_t)gridDim.x * blockDim.y) {
+      const double2 v = __ldg(x + g * b + r);
       a.x = fma(v.x, v.x, a.x);
       a.x = fma(v.y, v.y, a.x);
     }
@@ -171,10 +173,9 @@ __global__ void residual_kernel(int64_t n, int s, const double2* __restrict__ et
                                 GState g) {
   const int b = blockDim.x, rr = threadIdx.x;
   double2 a = make_double2(0.0, 0.0);
-  for (int64_t site = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; site < n;
-       site += (int64_t)gridDim.x * blockDim.y)
-    for (int k = 0; k < s; ++k) {
-      const int64_t i = ((int64_t)k * n + site) * b + rr;
+  const int64_t ng = groups(n, s);
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; g < ng; g += (int64_t)gridDim.x * blockDim.y) {
+      const int64_t i = g * b + rr;
       const double2 e = __ldg(eta + i), v = r[i];
       const double2 d = make_double2(e.x - v.x, e.y - v.y);
       r[i] = d;
@@ -218,10 +219,9 @@ __global__ void start_kernel(GState g) {
 __global__ void gdot_kernel(int64_t n, int s, const double2* __restrict__ z, const double2* __restrict__ w, GState g) {
   const int b = blockDim.x, r = threadIdx.x;
   double2 a = make_double2(0.0, 0.0);
-  for (int64_t site = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; site < n;
-       site += (int64_t)gridDim.x * blockDim.y)
-    for (int k = 0; k < s; ++k) {
-      const int64_t i = ((int64_t)k * n + site) * b + r;
+  const int64_t ng = groups(n, s);
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; g < ng; g += (int64_t)gridDim.x * blockDim.y) {
+      const int64_t i = g * b + r;
       acc_dot(a, __ldg(z + i), __ldg(w + i));
     }
   reduce_finish(a, g.sc, g.dot);
@@ -239,10 +239,9 @@ __global__ void mgs_kernel(int j, int p, int64_t n, int s, double2* __restrict__
   const double2 c = make_double2(-sig * hp.x, -sig * hp.y);  // w -= h_p V_p = h_p sigma_p Z_p
   if (blockIdx.x == 0 && threadIdx.y == 0) g.h_raw[((size_t)r * (m + 1) + p) * m + j] = hp;
   double2 a = make_double2(0.0, 0.0);
-  for (int64_t site = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; site < n;
-       site += (int64_t)gridDim.x * blockDim.y)
-    for (int k = 0; k < s; ++k) {
-      const int64_t i = ((int64_t)k * n + site) * b + r;
+  const int64_t ng = groups(n, s);
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; g < ng; g += (int64_t)gridDim.x * blockDim.y) {
+      const int64_t i = g * b + r;
       const double2 wn = cmac(w[i], c, __ldg(zp + i));
       w[i] = wn;
       if (NEXT) {
@@ -355,10 +354,9 @@ __global__ void update_kernel(int jd, int64_t n, int s, ZList zl, double2* __res
     const double sg = g.sigma[(size_t)p * g.b + r];
     coef[p] = make_double2(yp.x * sg, yp.y * sg);
   }
-  for (int64_t site = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; site < n;
-       site += (int64_t)gridDim.x * blockDim.y)
-    for (int k = 0; k < s; ++k) {
-      const int64_t i = ((int64_t)k * n + site) * b + r;
+  const int64_t ng = groups(n, s);
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; g < ng; g += (int64_t)gridDim.x * blockDim.y) {
+      const int64_t i = g * b + r;
       double2 a = psi[i];
 #pragma unroll 1
       for (int p = 0; p < jd; ++p) a = cmac(a, coef[p], __ldg(zl.z[p] + i));
@@ -406,7 +404,7 @@ extern "C" int b200wd_block_axpy(int64_t n_sites, int32_t s, int32_t b, const vo
                                  void* stream) {
   CHECK_FIELD(n_sites, s, b);
   B200WD_REQUIRE(alpha && x && y, "NULL pointer");
-  const int64_t total = n_sites * s * b;
+  const int64_t total = groups(n_sites, s) * b;
   int64_t g = (total + 255) / 256;
   if (g > 148 * 32) g = 148 * 32;
   axpy_kernel<<<(unsigned)g, 256, 0, as_stream(stream)>>>(total, b, static_cast<const double2*>(alpha),
@@ -417,7 +415,7 @@ extern "C" int b200wd_block_axpy(int64_t n_sites, int32_t s, int32_t b, const vo
 extern "C" int b200wd_block_scale(int64_t n_sites, int32_t s, int32_t b, const void* alpha, void* x, void* stream) {
   CHECK_FIELD(n_sites, s, b);
   B200WD_REQUIRE(alpha && x, "NULL pointer");
-  const int64_t total = n_sites * s * b;
+  const int64_t total = groups(n_sites, s) * b;
   int64_t g = (total + 255) / 256;
   if (g > 148 * 32) g = 148 * 32;
   scale_kernel<<<(unsigned)g, 256, 0, as_stream(stream)>>>(total, b, static_cast<const double2*>(alpha),

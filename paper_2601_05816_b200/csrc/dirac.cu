@@ -14,209 +14,49 @@
 // and finally writes  out = scale_r (alpha * xself + beta * H src)  once.
 // Neither lambda nor chi (the reference's 8 materialised half-spinor fields,
 // dirac.py:273-296) ever touches memory.
+#include <cstdlib>
+
 #include "capi.cuh"
 #include "common.cuh"
+#include "layout.cuh"
+#include "stencil.cuh"
 
 namespace b200wd {
 
-// A_mu blocks of the chiral basis as (permutation, unit phase code)
-// (projectors.py:40-48, 88-92).  Phase codes: 0:+1 1:+i 2:-1 3:-i.
-__host__ __device__ constexpr int a_perm(int mu, int s) { return (mu == 1 || mu == 2) ? 1 - s : s; }
-__host__ __device__ constexpr int a_code(int mu, int s) {
-  return mu == 0 ? 0 : mu == 1 ? 1 : mu == 2 ? (s == 0 ? 0 : 2) : (s == 0 ? 1 : 3);
-}
-// A_mu^H has the same permutation; its phases are the conjugates.
-__host__ __device__ constexpr int adj_code(int mu, int s) {
-  return mu == 0 ? 0 : mu == 1 ? 3 : mu == 2 ? (s == 0 ? 2 : 0) : (s == 0 ? 3 : 1);
-}
+// Threads per block of the hopping kernel and the occupancy target handed
+// to ptxas (c128: <= 168 registers -> 3 blocks = 12 warps per SM; c64: 4 blocks).
+constexpr int kHopThreads = 128;
+#ifndef B200WD_MINB_C128
+#define B200WD_MINB_C128 3
+#endif
+#ifndef B200WD_MINB_C64
+#define B200WD_MINB_C64 4
+#endif
+template <typename R> struct HopMinBlocks;
+template <> struct HopMinBlocks<double> { static constexpr int value = B200WD_MINB_C128; };
+template <> struct HopMinBlocks<float> { static constexpr int value = B200WD_MINB_C64; };
 
-struct HopParams {
-  int32_t T, X, Y, Z;
-  int32_t par0;        // parity of local slice 0 (t_origin & 1)
-  int32_t b;           // rhs count
-  int32_t dst_parity;  // -1: full lattice
-  int64_t n;           // local sites
-  int64_t n_src, n_dst;
-  int64_t d_begin, d_end;  // destination index range in the dst field
-  int64_t per_t;           // X*Y*Z
-  int64_t nf;              // face sites of the src field
-  const void* U;
-  const void* src;
-  const void* xself;
-  void* out;
-  double alpha, beta;  // beta carries the 1/2 of the projectors
-  const double* scale;
-  const void* lam_halo;
-  const void* chi_halo;
-};
-
-// ---- V-wide loads/stores of consecutive rhs ---------------------------------
-template <typename R, int V> struct VecIO;
-template <> struct VecIO<double, 1> {
-  static __device__ __forceinline__ void ld(double2 (&o)[1], const double2* p) { o[0] = __ldg(p); }
-  static __device__ __forceinline__ void st(double2* p, const double2 (&v)[1]) { __stcs(p, v[0]); }
-};
-template <> struct VecIO<float, 1> {
-  static __device__ __forceinline__ void ld(float2 (&o)[1], const float2* p) { o[0] = __ldg(p); }
-  static __device__ __forceinline__ void st(float2* p, const float2 (&v)[1]) { __stcs(p, v[0]); }
-};
-template <> struct VecIO<float, 2> {
-  static __device__ __forceinline__ void ld(float2 (&o)[2], const float2* p) {
-    float4 q = __ldg(reinterpret_cast<const float4*>(p));
-    o[0] = make_float2(q.x, q.y);
-    o[1] = make_float2(q.z, q.w);
-  }
-  static __device__ __forceinline__ void st(float2* p, const float2 (&v)[2]) {
-    __stcs(reinterpret_cast<float4*>(p), make_float4(v[0].x, v[0].y, v[1].x, v[1].y));
-  }
-};
-
-// g = M h for the two colour vectors, M = U (DAG=false) or U^H (DAG=true).
-template <bool DAG>
-__device__ __forceinline__ void matvec2(double2 (&g)[2][3], const double2 (&u)[9],
-                                        const double2 (&h)[2][3]) {
-#pragma unroll
-  for (int s = 0; s < 2; ++s)
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      double2 a = mk(0.0, 0.0);
-#pragma unroll
-      for (int j = 0; j < 3; ++j) a = DAG ? cmacc(a, u[3 * j + i], h[s][j]) : cmac(a, u[3 * i + j], h[s][j]);
-      g[s][i] = a;
-    }
-}
-template <bool DAG>
-__device__ __forceinline__ void matvec2(float2 (&g)[2][3], const float2 (&u)[9], const float2 (&h)[2][3]) {
-#pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    float2 hs[3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) hs[j] = mk(-h[s][j].y, h[s][j].x);
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      float2 a = mk(0.f, 0.f);
-#pragma unroll
-      for (int j = 0; j < 3; ++j)
-        a = DAG ? cmacc_s(a, u[3 * j + i], h[s][j], hs[j]) : cmac_s(a, u[3 * i + j], h[s][j], hs[j]);
-      g[s][i] = a;
-    }
-  }
-}
-
-// h_s = u_s - sign * A_mu l_s without the 1/2 (projectors.py:126-136);
-// FWD is the sign -1 (lambda) projection, !FWD the sign +1 (chi) one.
-template <int MU, bool FWD, int S, typename C>
-__device__ __forceinline__ void project_spin(C (&h)[3], const C (&psi)[12]) {
-  constexpr int code = FWD ? a_code(MU, S) : ((a_code(MU, S) + 2) & 3);
-  constexpr int lp = 6 + 3 * a_perm(MU, S);
-#pragma unroll
-  for (int c = 0; c < 3; ++c) h[c] = cadd(psi[3 * S + c], phase<code>(psi[lp + c]));
-}
-
-// acc += reconstruct(g) for sign -1 (FWD: lower += A^H g) or +1 (lower -= A^H g)
-// (projectors.py:144-147, dirac.py:258-263)
-template <int MU, bool FWD, int S, typename C>
-__device__ __forceinline__ void accumulate_spin(C (&acc)[12], const C (&g)[2][3]) {
-  constexpr int code = FWD ? adj_code(MU, S) : ((adj_code(MU, S) + 2) & 3);
-  constexpr int gp = a_perm(MU, S);
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    acc[3 * S + c] = cadd(acc[3 * S + c], g[S][c]);
-    acc[6 + 3 * S + c] = cadd(acc[6 + 3 * S + c], phase<code>(g[gp][c]));
-  }
-}
-
-// One hop from a full neighbour spinor (12 components loaded from src).
-template <int MU, bool FWD, typename R, int V>
-__device__ __forceinline__ void hop_full(cx<R> (&acc)[V][12], const cx<R>* __restrict__ sp, int64_t kstride,
-                                         const cx<R>* __restrict__ up, int64_t estride) {
-  using C = cx<R>;
-  C psi[V][12];
-#pragma unroll
-  for (int k = 0; k < 12; ++k) {
-    C tmp[V];
-    VecIO<R, V>::ld(tmp, sp + k * kstride);
-#pragma unroll
-    for (int v = 0; v < V; ++v) psi[v][k] = tmp[v];
-  }
-  C u[9];
-#pragma unroll
-  for (int e = 0; e < 9; ++e) u[e] = __ldg(up + e * estride);
-#pragma unroll
-  for (int v = 0; v < V; ++v) {
-    C h[2][3], g[2][3];
-    project_spin<MU, FWD, 0>(h[0], psi[v]);
-    project_spin<MU, FWD, 1>(h[1], psi[v]);
-    matvec2<!FWD>(g, u, h);
-    accumulate_spin<MU, FWD, 0>(acc[v], g);
-    accumulate_spin<MU, FWD, 1>(acc[v], g);
-  }
-}
-
-// Forward T hop whose projected half spinor comes from the lam halo face.
-template <typename R, int V>
-__device__ __forceinline__ void hop_lam_halo(cx<R> (&acc)[V][12], const cx<R>* __restrict__ hp, int64_t hstride,
-                                             const cx<R>* __restrict__ up, int64_t estride) {
-  using C = cx<R>;
-  C hh[V][6];
-#pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    C tmp[V];
-    VecIO<R, V>::ld(tmp, hp + k * hstride);
-#pragma unroll
-    for (int v = 0; v < V; ++v) hh[v][k] = tmp[v];
-  }
-  C u[9];
-#pragma unroll
-  for (int e = 0; e < 9; ++e) u[e] = __ldg(up + e * estride);
-#pragma unroll
-  for (int v = 0; v < V; ++v) {
-    C h[2][3], g[2][3];
-#pragma unroll
-    for (int s = 0; s < 2; ++s)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) h[s][c] = hh[v][3 * s + c];
-    matvec2<false>(g, u, h);
-    accumulate_spin<0, true, 0>(acc[v], g);
-    accumulate_spin<0, true, 1>(acc[v], g);
-  }
-}
-
-// Backward T hop whose U^H-multiplied half spinor comes from the chi face.
-template <typename R, int V>
-__device__ __forceinline__ void hop_chi_halo(cx<R> (&acc)[V][12], const cx<R>* __restrict__ hp, int64_t hstride) {
-  using C = cx<R>;
-#pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    C tmp[V];
-    VecIO<R, V>::ld(tmp, hp + k * hstride);
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      // sign +1 reconstruction with A_0 = I: upper += g, lower -= g
-      acc[v][k] = cadd(acc[v][k], tmp[v]);
-      acc[v][6 + k] = csub(acc[v][6 + k], tmp[v]);
-    }
-  }
-}
-
-template <typename R, int V, bool PAR, bool HALO>
-__global__ void __launch_bounds__(256) hop_kernel(const HopParams p) {
+// B > 0: rhs count known at compile time (all component / link strides are
+// immediates); B == 0: runtime rhs count.
+template <typename R, int V, int B>
+__global__ void __launch_bounds__(kHopThreads, HopMinBlocks<R>::value) hop_kernel(const HopParams p) {
   using C = cx<R>;
   const int64_t d = p.d_begin + (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
   if (d >= p.d_end) return;
+  const int b = B > 0 ? B : p.b;
   const int r0 = threadIdx.x * V;
-  const int b = p.b;
   const int Z = p.Z, Y = p.Y, X = p.X, T = p.T;
+  const bool par = p.dst_parity >= 0;
 
   // natural site and its coordinates (geometry.py:51-72)
-  int64_t site = PAR ? 2 * d : d;
+  int64_t site = par ? 2 * d : d;
   int z = (int)(site % Z);
   int64_t q = site / Z;
   const int y = (int)(q % Y);
   q /= Y;
   const int x = (int)(q % X);
   const int t = (int)(q / X);
-  if (PAR) {
+  if (par) {
     const int zz = z + ((t + x + y + z + p.par0 + p.dst_parity) & 1);
     site += zz - z;
     z = zz;
@@ -225,8 +65,7 @@ __global__ void __launch_bounds__(256) hop_kernel(const HopParams p) {
 
   const C* __restrict__ src = static_cast<const C*>(p.src);
   const C* __restrict__ U = static_cast<const C*>(p.U);
-  const int64_t kstride = p.n_src * b;
-  const int64_t n = p.n;
+  const int kst = 8 * b;  // component stride (elements)
 
   C acc[V][12];
 #pragma unroll
@@ -234,24 +73,29 @@ __global__ void __launch_bounds__(256) hop_kernel(const HopParams p) {
 #pragma unroll
     for (int k = 0; k < 12; ++k) acc[v][k] = mk(R(0), R(0));
 
-  auto sidx = [&](int64_t s) -> int64_t { return PAR ? (s >> 1) : s; };
-  auto sptr = [&](int64_t s) { return src + sidx(s) * b + r0; };
+  auto sptr = [&](int64_t s) {
+    const int64_t i = par ? (s >> 1) : s;
+    return src + spinor_base(i, 12, b) + r0;
+  };
+  const bool halo = p.lam_halo != nullptr;
 
   // forward hops: P-_mu U_mu(x) psi(x+mu)  (dirac.py:222-245)
   {
+    const C* ux = U + link_base(site);
     const int64_t f3 = (z + 1 == Z) ? site - (Z - 1) : site + 1;
     const int64_t f2 = (y + 1 == Y) ? site - (int64_t)(Y - 1) * sY : site + sY;
     const int64_t f1 = (x + 1 == X) ? site - (int64_t)(X - 1) * sX : site + sX;
     const int64_t f0 = (t + 1 == T) ? site - (int64_t)(T - 1) * sT : site + sT;
-    if (HALO && t + 1 == T) {
-      const C* hp = static_cast<const C*>(p.lam_halo) + sidx(f0) * b + r0;
-      hop_lam_halo<R, V>(acc, hp, p.nf * b, U + 0 * 9 * n + site, n);
+    if (halo && t + 1 == T) {
+      const int64_t fi = par ? (f0 >> 1) : f0;
+      const C* hp = static_cast<const C*>(p.lam_halo) + fi * b + r0;
+      hop_lam_halo<R, V>(acc, hp, p.nf * b, ux + 0 * 72, 8);
     } else {
-      hop_full<0, true, R, V>(acc, sptr(f0), kstride, U + 0 * 9 * n + site, n);
+      hop_full<0, true, R, V>(acc, sptr(f0), kst, ux + 0 * 72, 8);
     }
-    hop_full<1, true, R, V>(acc, sptr(f1), kstride, U + 1 * 9 * n + site, n);
-    hop_full<2, true, R, V>(acc, sptr(f2), kstride, U + 2 * 9 * n + site, n);
-    hop_full<3, true, R, V>(acc, sptr(f3), kstride, U + 3 * 9 * n + site, n);
+    hop_full<1, true, R, V>(acc, sptr(f1), kst, ux + 1 * 72, 8);
+    hop_full<2, true, R, V>(acc, sptr(f2), kst, ux + 2 * 72, 8);
+    hop_full<3, true, R, V>(acc, sptr(f3), kst, ux + 3 * 72, 8);
   }
   // backward hops: P+_mu U_mu(x-mu)^H psi(x-mu)  (dirac.py:185-219, 248-255)
   {
@@ -259,21 +103,22 @@ __global__ void __launch_bounds__(256) hop_kernel(const HopParams p) {
     const int64_t b2 = (y == 0) ? site + (int64_t)(Y - 1) * sY : site - sY;
     const int64_t b1 = (x == 0) ? site + (int64_t)(X - 1) * sX : site - sX;
     const int64_t b0 = (t == 0) ? site + (int64_t)(T - 1) * sT : site - sT;
-    if (HALO && t == 0) {
-      const C* hp = static_cast<const C*>(p.chi_halo) + sidx(site) * b + r0;
+    if (halo && t == 0) {
+      const int64_t fi = par ? (site >> 1) : site;
+      const C* hp = static_cast<const C*>(p.chi_halo) + fi * b + r0;
       hop_chi_halo<R, V>(acc, hp, p.nf * b);
     } else {
-      hop_full<0, false, R, V>(acc, sptr(b0), kstride, U + 0 * 9 * n + b0, n);
+      hop_full<0, false, R, V>(acc, sptr(b0), kst, U + link_base(b0) + 0 * 72, 8);
     }
-    hop_full<1, false, R, V>(acc, sptr(b1), kstride, U + 1 * 9 * n + b1, n);
-    hop_full<2, false, R, V>(acc, sptr(b2), kstride, U + 2 * 9 * n + b2, n);
-    hop_full<3, false, R, V>(acc, sptr(b3), kstride, U + 3 * 9 * n + b3, n);
+    hop_full<1, false, R, V>(acc, sptr(b1), kst, U + link_base(b1) + 1 * 72, 8);
+    hop_full<2, false, R, V>(acc, sptr(b2), kst, U + link_base(b2) + 2 * 72, 8);
+    hop_full<3, false, R, V>(acc, sptr(b3), kst, U + link_base(b3) + 3 * 72, 8);
   }
 
   // epilogue: out = scale_r (alpha xself + beta acc)
-  const int64_t okstride = p.n_dst * b;
-  C* out = static_cast<C*>(p.out) + d * b + r0;
-  const C* xs = static_cast<const C*>(p.xself);
+  const int64_t o = spinor_base(d, 12, b) + r0;
+  C* out = static_cast<C*>(p.out) + o;
+  const C* xs = p.xself ? static_cast<const C*>(p.xself) + o : nullptr;
   R sc[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) sc[v] = p.scale ? R(__ldg(p.scale + r0 + v)) : R(1);
@@ -283,7 +128,7 @@ __global__ void __launch_bounds__(256) hop_kernel(const HopParams p) {
     C res[V];
     if (xs) {
       C xv[V];
-      VecIO<R, V>::ld(xv, xs + d * b + r0 + k * okstride);
+      VecIO<R, V>::ld(xv, xs + k * kst);
 #pragma unroll
       for (int v = 0; v < V; ++v)
         res[v] = mk(sc[v] * (alpha * xv[v].x + beta * acc[v][k].x), sc[v] * (alpha * xv[v].y + beta * acc[v][k].y));
@@ -291,30 +136,312 @@ __global__ void __launch_bounds__(256) hop_kernel(const HopParams p) {
 #pragma unroll
       for (int v = 0; v < V; ++v) res[v] = mk(sc[v] * beta * acc[v][k].x, sc[v] * beta * acc[v][k].y);
     }
-    VecIO<R, V>::st(out + k * okstride, res);
+    VecIO<R, V>::st(out + k * kst, res);
   }
 }
 
+// ---- persistent TMA ring kernel (full lattice) ---------------------------------
+//
+// Warp-specialised, persistent: one producer warp per CTA streams the inputs
+// of consecutive work items (NB site blocks of 8 z-consecutive sites x all b
+// rhs) into shared memory with cp.async.bulk (TMA 1-D bulk copies),
+// completion counted by mbarrier transactions; the consumer warps compute
+// from shared memory and hand each slot back through an "empty" mbarrier.
+// For the t, x and y hops the 8 neighbours of a site block are exactly one
+// other site block (Z % 8 == 0), i.e. one contiguous 96*b-complex run, so a
+// hop tile is NB bulk copies of spinor blocks + NB copies of one 72-complex
+// link plane (U_mu of the own block for forward hops, of the neighbour block
+// for backward hops).  Each item streams 6 hop tiles through an S-slot ring,
+// then its own block ("z tile": z hops + the xself of the epilogue) through
+// a dedicated buffer.  Loads in flight live in shared memory, not registers,
+// so the bytes in flight per SM (Little's law) are set by the ring depth.
+template <typename R, int V, int B> struct RingShape {
+  static constexpr int BT = B / V;                                   // threads per site
+  static constexpr int NB = (BT * 8 >= 96) ? 1 : (128 / (BT * 8));   // site blocks per item
+  static constexpr int NC = BT * 8 * NB;                             // consumer threads
+  static constexpr int NCW = NC / 32;                                // consumer warps
+  static constexpr int NT = NC + 32;                                 // + producer warp
+  static constexpr int SPIN = NB * 96 * B;                           // complex per spinor tile
+  static constexpr int SLOT = SPIN + NB * 72;                        // + one link plane per block
+  static constexpr int SLOT_BYTES = SLOT * (int)sizeof(cx<R>);
+  static constexpr int S = SLOT_BYTES <= 28 * 1024 ? 3 : 2;          // hop-ring depth
+  static constexpr size_t SMEM = (size_t)SLOT_BYTES * (S + 1) + 8 * 2 * (S + 1);
+};
+
+// Coordinates of the first site of a site block (32-bit arithmetic: a rank's
+// local lattice has < 2^31 sites).
+struct BlkCoord {
+  int t, x, y, z0;
+};
+__device__ __forceinline__ BlkCoord block_coord(int64_t g, const HopParams& p) {
+  uint32_t s0 = (uint32_t)(g * 8);
+  BlkCoord c;
+  c.z0 = (int)(s0 % (uint32_t)p.Z);
+  s0 /= (uint32_t)p.Z;
+  c.y = (int)(s0 % (uint32_t)p.Y);
+  s0 /= (uint32_t)p.Y;
+  c.x = (int)(s0 % (uint32_t)p.X);
+  c.t = (int)(s0 / (uint32_t)p.X);
+  return c;
+}
+// step to the next site block (z0 += 8 with carries)
+__device__ __forceinline__ void block_step(BlkCoord& c, const HopParams& p) {
+  c.z0 += 8;
+  if (c.z0 == p.Z) {
+    c.z0 = 0;
+    if (++c.y == p.Y) {
+      c.y = 0;
+      if (++c.x == p.X) {
+        c.x = 0;
+        ++c.t;
+      }
+    }
+  }
+}
+
+template <int MU, bool FWD>
+__device__ __forceinline__ int64_t block_neighbor(int64_t g, const BlkCoord& c, const HopParams& p) {
+  const int64_t s0 = g * 8;
+  const int64_t sY = p.Z, sX = (int64_t)p.Y * p.Z, sT = p.per_t;
+  int64_t ns;
+  if constexpr (MU == 0) ns = FWD ? (c.t + 1 == p.T ? s0 - (int64_t)(p.T - 1) * sT : s0 + sT)
+                                  : (c.t == 0 ? s0 + (int64_t)(p.T - 1) * sT : s0 - sT);
+  else if constexpr (MU == 1) ns = FWD ? (c.x + 1 == p.X ? s0 - (int64_t)(p.X - 1) * sX : s0 + sX)
+                                       : (c.x == 0 ? s0 + (int64_t)(p.X - 1) * sX : s0 - sX);
+  else ns = FWD ? (c.y + 1 == p.Y ? s0 - (int64_t)(p.Y - 1) * sY : s0 + sY)
+                : (c.y == 0 ? s0 + (int64_t)(p.Y - 1) * sY : s0 - sY);
+  return ns >> 3;
+}
+
+// tile H in 0..5: hop (mu = H/2, forward if H even); H == 6: own block (z tile)
+template <typename R, int V, int B, int H>
+__device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, BlkCoord c, cx<R>* slot,
+                                           uint64_t* full) {
+  using C = cx<R>;
+  using Sh = RingShape<R, V, B>;
+  constexpr uint32_t bytes = (uint32_t)(Sh::SLOT * sizeof(C));
+  mbar_expect_tx(full, bytes);
+  const C* src = static_cast<const C*>(p.src);
+  const C* U = static_cast<const C*>(p.U);
+#pragma unroll
+  for (int jj = 0; jj < Sh::NB; ++jj) {
+    const int64_t g = gb0 + jj;
+    int64_t nb = g, lb = g;
+    int mu = 3;
+    if constexpr (H < 6) {
+      constexpr int MU = H >> 1;
+      constexpr bool FWD = !(H & 1);
+      mu = MU;
+      nb = block_neighbor<MU, FWD>(g, c, p);
+      lb = FWD ? g : nb;
+    }
+    bulk_g2s(slot + jj * 96 * B, src + nb * 96 * B, 96 * B * sizeof(C), full);
+    bulk_g2s(slot + Sh::SPIN + jj * 72, U + lb * 288 + mu * 72, 72 * sizeof(C), full);
+    if (jj + 1 < Sh::NB) block_step(c, p);
+  }
+}
+
+template <typename R, int V, int B>
+__global__ void __launch_bounds__(RingShape<R, V, B>::NT) hop_ring_kernel(const HopParams p, int64_t n_items) {
+  using C = cx<R>;
+  using Sh = RingShape<R, V, B>;
+  constexpr int S = Sh::S;
+  constexpr int KST = 8 * B;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  C* ring = reinterpret_cast<C*>(smem_raw);
+  C* zbuf = ring + S * Sh::SLOT;
+  uint64_t* full = reinterpret_cast<uint64_t*>(zbuf + Sh::SLOT);  // [S] ring + [1] z
+  uint64_t* empty = full + (S + 1);
+
+  const int tid = threadIdx.x;  // 1-D block: consumers [0, NC), producer warp [NC, NC+32)
+  const bool producer = tid >= Sh::NC;
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i <= S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], Sh::NCW);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (producer) {
+    if (tid == Sh::NC) {  // one elected lane issues every copy
+      int seq = 0, zuse = 0;
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int64_t gb0 = (p.d_begin >> 3) + it * Sh::NB;
+        const BlkCoord c0 = block_coord(gb0, p);
+#define B200WD_PRODUCE(H)                                                                 \
+  {                                                                                       \
+    const int slot = seq % S, use = seq / S;                                              \
+    if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);                                  \
+    ring_issue<R, V, B, H>(p, gb0, c0, ring + slot * Sh::SLOT, &full[slot]);              \
+    ++seq;                                                                                \
+  }
+        B200WD_PRODUCE(0)
+        B200WD_PRODUCE(1)
+        B200WD_PRODUCE(2)
+        B200WD_PRODUCE(3)
+        B200WD_PRODUCE(4)
+        B200WD_PRODUCE(5)
+#undef B200WD_PRODUCE
+        if (zuse > 0) mbar_wait(&empty[S], (zuse - 1) & 1);
+        ring_issue<R, V, B, 6>(p, gb0, c0, zbuf, &full[S]);
+        ++zuse;
+      }
+    }
+    return;
+  }
+
+  // ---- consumers ----
+  const int r0 = (tid % Sh::BT) * V;
+  const int ysite = tid / Sh::BT;
+  const int j = ysite >> 3, lo = ysite & 7;
+  const bool lead = (tid & 31) == 0;
+  const C* __restrict__ src = static_cast<const C*>(p.src);
+  const C* __restrict__ U = static_cast<const C*>(p.U);
+  const int Z = p.Z;
+  R sc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) sc[v] = p.scale ? R(__ldg(p.scale + r0 + v)) : R(1);
+  const R beta = R(p.beta), alpha = R(p.alpha);
+  const bool self_is_src = p.xself == p.src;
+
+  int seq = 0, zuse = 0;
+  for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int64_t gb0 = (p.d_begin >> 3) + it * Sh::NB;
+    const int64_t d = (gb0 + j) * 8 + lo;
+    C acc[V][12];
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int k = 0; k < 12; ++k) acc[v][k] = mk(R(0), R(0));
+
+#define B200WD_CONSUME(H)                                                                            \
+  {                                                                                                  \
+    const int slot = seq % S;                                                                        \
+    mbar_wait(&full[slot], (seq / S) & 1);                                                           \
+    const C* sb = ring + slot * Sh::SLOT;                                                            \
+    hop_full<((H) >> 1), !((H)&1), R, V, true, true>(acc, sb + j * 96 * B + lo * B + r0, KST,        \
+                                                      sb + Sh::SPIN + j * 72 + lo, 8);               \
+    __syncwarp();                                                                                    \
+    if (lead) mbar_arrive(&empty[slot]);                                                             \
+    ++seq;                                                                                           \
+  }
+    B200WD_CONSUME(0)
+    B200WD_CONSUME(1)
+    B200WD_CONSUME(2)
+    B200WD_CONSUME(3)
+    B200WD_CONSUME(4)
+    B200WD_CONSUME(5)
+#undef B200WD_CONSUME
+
+    // z hops from the own block; edge sites of a z line come from global memory
+    mbar_wait(&full[S], zuse & 1);
+    const int z = (int)((uint32_t)d % (uint32_t)Z);
+    {
+      const int64_t nd = (z + 1 == Z) ? d - (Z - 1) : d + 1;
+      const int64_t jb = (nd >> 3) - gb0;
+      const C* ul = zbuf + Sh::SPIN + j * 72 + lo;  // U_3(x) of the own block
+      if (jb >= 0 && jb < Sh::NB)
+        hop_full<3, true, R, V, true, true>(acc, zbuf + jb * 96 * B + (nd & 7) * B + r0, KST, ul, 8);
+      else
+        hop_full<3, true, R, V, false, true>(acc, src + spinor_base(nd, 12, B) + r0, KST, ul, 8);
+    }
+    {
+      const int64_t nd = (z == 0) ? d + (Z - 1) : d - 1;
+      const int64_t jb = (nd >> 3) - gb0;
+      if (jb >= 0 && jb < Sh::NB)
+        hop_full<3, false, R, V, true, true>(acc, zbuf + jb * 96 * B + (nd & 7) * B + r0, KST,
+                                             zbuf + Sh::SPIN + jb * 72 + (nd & 7), 8);
+      else
+        hop_full<3, false, R, V, false, false>(acc, src + spinor_base(nd, 12, B) + r0, KST,
+                                               U + link_base(nd) + 3 * 72, 8);
+    }
+    // epilogue: out = scale_r (alpha xself + beta acc)
+    const int64_t o = spinor_base(d, 12, B) + r0;
+    C* out = static_cast<C*>(p.out) + o;
+    const C* xs = p.xself ? static_cast<const C*>(p.xself) + o : nullptr;
+    const C* xz = zbuf + j * 96 * B + lo * B + r0;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+      C res[V];
+      if (xs) {
+        C xv[V];
+        if (self_is_src) VecIO<R, V>::lds(xv, xz + k * KST);
+        else VecIO<R, V>::ld(xv, xs + k * KST);
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          res[v] = mk(sc[v] * (alpha * xv[v].x + beta * acc[v][k].x), sc[v] * (alpha * xv[v].y + beta * acc[v][k].y));
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) res[v] = mk(sc[v] * beta * acc[v][k].x, sc[v] * beta * acc[v][k].y);
+      }
+      VecIO<R, V>::st(out + k * KST, res);
+    }
+    __syncwarp();
+    if (lead) mbar_arrive(&empty[S]);
+    ++zuse;
+  }
+}
+
+static int g_sm_count = 0;
+
+// Launch the ring kernel when its shape preconditions hold; false -> the
+// caller uses the generic kernel.
+template <typename R, int V, int B>
+static bool try_launch_ring(const HopParams& p, cudaStream_t st) {
+  using Sh = RingShape<R, V, B>;
+  if (Sh::NC % 32 != 0) return false;
+  if (p.dst_parity >= 0 || p.lam_halo != nullptr || p.Z % 8 != 0) return false;
+  if ((p.d_begin & 7) || (p.d_end & 7)) return false;
+  const int64_t nblk = (p.d_end - p.d_begin) >> 3;
+  if (nblk % Sh::NB) return false;
+  static int ctas_per_sm = -1;
+  if (ctas_per_sm < 0) {
+    if (cudaFuncSetAttribute(hop_ring_kernel<R, V, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)Sh::SMEM) != cudaSuccess) {
+      ctas_per_sm = 0;
+      return false;
+    }
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, hop_ring_kernel<R, V, B>, Sh::NT, Sh::SMEM) != cudaSuccess)
+      nb = 0;
+    ctas_per_sm = nb;
+    if (g_sm_count == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+    }
+  }
+  if (ctas_per_sm <= 0) return false;
+  const int64_t n_items = nblk / Sh::NB;
+  int64_t grid = (int64_t)ctas_per_sm * g_sm_count;
+  if (grid > n_items) grid = n_items;
+  hop_ring_kernel<R, V, B><<<(unsigned)grid, Sh::NT, Sh::SMEM, st>>>(p, n_items);
+  return true;
+}
+
 // ---- halo face pack (halo.py:352-368) ---------------------------------------
-template <typename R, int V, bool PAR>
+template <typename R, int V>
 __global__ void __launch_bounds__(256) halo_pack_kernel(const HopParams p, void* lam_face, void* chi_face) {
   using C = cx<R>;
   const int64_t i = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;  // face index
   if (i >= p.nf) return;
   const int r0 = threadIdx.x * V;
   const int b = p.b;
+  const bool par = p.dst_parity >= 0;  // parity of the source field
   const C* __restrict__ src = static_cast<const C*>(p.src);
   const C* __restrict__ U = static_cast<const C*>(p.U);
-  const int64_t kstride = p.n_src * b;
+  const int kst = 8 * b;
   const int64_t fstride = p.nf * b;
-  // src parity for PAR is p.dst_parity (reused field)
   for (int face = 0; face < 2; ++face) {
     const int tf = face == 0 ? 0 : p.T - 1;
-    int64_t sidx = PAR ? i + (int64_t)tf * (p.per_t / 2) : i + (int64_t)tf * p.per_t;
+    const int64_t sidx = par ? i + (int64_t)tf * (p.per_t / 2) : i + (int64_t)tf * p.per_t;
     int64_t site = sidx;
-    if (PAR) {
+    if (par) {
       site = 2 * sidx;
-      int z = (int)(site % p.Z);
+      const int z = (int)(site % p.Z);
       int64_t q = site / p.Z;
       const int y = (int)(q % p.Y);
       q /= p.Y;
@@ -322,11 +449,12 @@ __global__ void __launch_bounds__(256) halo_pack_kernel(const HopParams p, void*
       const int t = (int)(q / p.X);
       site += (t + x + y + z + p.par0 + p.dst_parity) & 1;
     }
+    const C* sp = src + spinor_base(sidx, 12, b) + r0;
     C psi[V][12];
 #pragma unroll
     for (int k = 0; k < 12; ++k) {
       C tmp[V];
-      VecIO<R, V>::ld(tmp, src + sidx * b + r0 + k * kstride);
+      VecIO<R, V>::ld(tmp, sp + k * kst);
 #pragma unroll
       for (int v = 0; v < V; ++v) psi[v][k] = tmp[v];
     }
@@ -340,9 +468,10 @@ __global__ void __launch_bounds__(256) halo_pack_kernel(const HopParams p, void*
         VecIO<R, V>::st(out + hk * fstride, res);
       }
     } else {
+      const C* ux = U + link_base(site);
       C u[9];
 #pragma unroll
-      for (int e = 0; e < 9; ++e) u[e] = __ldg(U + (int64_t)e * p.n + site);
+      for (int e = 0; e < 9; ++e) u[e] = __ldg(ux + e * 8);
       C g[V][2][3];
 #pragma unroll
       for (int v = 0; v < V; ++v) {
@@ -363,30 +492,67 @@ __global__ void __launch_bounds__(256) halo_pack_kernel(const HopParams p, void*
   }
 }
 
-template <typename R, int V>
-static void launch_hop(const HopParams& p, bool par, bool halo, cudaStream_t st) {
-  const int bt = p.b / V;
-  const int S = bt >= 256 ? 1 : 256 / bt;
+static bool bulk_enabled() {
+  static int en = -1;
+  if (en < 0) {
+    const char* e = getenv("B200WD_NO_TMA");
+    en = (e && e[0] == '1') ? 0 : 1;
+  }
+  return en == 1;
+}
+
+template <typename R, int V, int B>
+static void launch_hop_b(const HopParams& p, cudaStream_t st) {
+  if constexpr (B >= 4) {
+    if (bulk_enabled() && try_launch_ring<R, V, B>(p, st)) return;
+  }
+  const int bt = (B > 0 ? B : p.b) / V;
+  const int S = bt >= kHopThreads ? 1 : kHopThreads / bt;
   dim3 block(bt, S);
   const int64_t nd = p.d_end - p.d_begin;
   dim3 grid((unsigned)((nd + S - 1) / S));
-  if (par) {
-    if (halo) hop_kernel<R, V, true, true><<<grid, block, 0, st>>>(p);
-    else hop_kernel<R, V, true, false><<<grid, block, 0, st>>>(p);
-  } else {
-    if (halo) hop_kernel<R, V, false, true><<<grid, block, 0, st>>>(p);
-    else hop_kernel<R, V, false, false><<<grid, block, 0, st>>>(p);
-  }
+  hop_kernel<R, V, B><<<grid, block, 0, st>>>(p);
+}
+
+// compile-time rhs counts that get their own instantiation per (R, V)
+template <typename R, int V> __host__ __device__ constexpr bool wanted_b(int bb) {
+  return bb % V == 0 && (V == 2 || sizeof(R) == 8 || bb % 2 == 1);
 }
 
 template <typename R, int V>
-static void launch_pack(const HopParams& p, bool par, void* lam, void* chi, cudaStream_t st) {
+static void launch_hop(const HopParams& p, cudaStream_t st) {
+  switch (p.b) {
+#define B200WD_CASE(BB)                       \
+  case BB:                                    \
+    if constexpr (wanted_b<R, V>(BB)) {       \
+      launch_hop_b<R, V, BB>(p, st);          \
+      return;                                 \
+    }                                         \
+    break;
+    B200WD_CASE(1)
+    B200WD_CASE(2)
+    B200WD_CASE(3)
+    B200WD_CASE(4)
+    B200WD_CASE(6)
+    B200WD_CASE(8)
+    B200WD_CASE(12)
+    B200WD_CASE(16)
+    B200WD_CASE(24)
+    B200WD_CASE(32)
+#undef B200WD_CASE
+    default:
+      break;
+  }
+  launch_hop_b<R, V, 0>(p, st);
+}
+
+template <typename R, int V>
+static void launch_pack(const HopParams& p, void* lam, void* chi, cudaStream_t st) {
   const int bt = p.b / V;
   const int S = bt >= 256 ? 1 : 256 / bt;
   dim3 block(bt, S);
   dim3 grid((unsigned)((p.nf + S - 1) / S));
-  if (par) halo_pack_kernel<R, V, true><<<grid, block, 0, st>>>(p, lam, chi);
-  else halo_pack_kernel<R, V, false><<<grid, block, 0, st>>>(p, lam, chi);
+  halo_pack_kernel<R, V><<<grid, block, 0, st>>>(p, lam, chi);
 }
 
 static int fill_params(HopParams& p, const b200wd_lattice* lat, int32_t dtype, int32_t b, int32_t parity) {
@@ -395,7 +561,7 @@ static int fill_params(HopParams& p, const b200wd_lattice* lat, int32_t dtype, i
     B200WD_REQUIRE(lat->dims[d] >= 2 && lat->dims[d] % 2 == 0,
                    "extent %d in direction %d is not an even number >= 2", lat->dims[d], d);
   B200WD_REQUIRE(dtype == B200WD_C128 || dtype == B200WD_C64, "unknown dtype %d", dtype);
-  B200WD_REQUIRE(b >= 1 && b <= 256, "rhs count b=%d out of range [1,256]", b);
+  B200WD_REQUIRE(b >= 1 && b <= 128, "rhs count b=%d out of range [1,128]", b);
   B200WD_REQUIRE(parity >= -1 && parity <= 1, "parity must be -1, 0 or 1 (got %d)", parity);
   B200WD_REQUIRE((lat->t_origin & 1) == 0, "t_origin must be even (got %d)", lat->t_origin);
   p = HopParams{};
@@ -441,14 +607,13 @@ extern "C" int b200wd_hop(const b200wd_lattice* lat, int32_t dtype, int32_t b, i
   const int64_t per = dst_parity < 0 ? p.per_t : p.per_t / 2;
   p.d_begin = per * t_begin;
   p.d_end = per * t_end;
-  const bool halo = lam_halo != nullptr;
   cudaStream_t st = as_stream(stream);
   if (dtype == B200WD_C128) {
-    launch_hop<double, 1>(p, dst_parity >= 0, halo, st);
+    launch_hop<double, 1>(p, st);
   } else if (b % 2 == 0) {
-    launch_hop<float, 2>(p, dst_parity >= 0, halo, st);
+    launch_hop<float, 2>(p, st);
   } else {
-    launch_hop<float, 1>(p, dst_parity >= 0, halo, st);
+    launch_hop<float, 1>(p, st);
   }
   return check_launch("b200wd_hop");
 }
@@ -469,8 +634,8 @@ extern "C" int b200wd_halo_pack(const b200wd_lattice* lat, int32_t dtype, int32_
   p.U = links;
   p.src = src;
   cudaStream_t st = as_stream(stream);
-  if (dtype == B200WD_C128) launch_pack<double, 1>(p, src_parity >= 0, lam_face, chi_face, st);
-  else if (b % 2 == 0) launch_pack<float, 2>(p, src_parity >= 0, lam_face, chi_face, st);
-  else launch_pack<float, 1>(p, src_parity >= 0, lam_face, chi_face, st);
+  if (dtype == B200WD_C128) launch_pack<double, 1>(p, lam_face, chi_face, st);
+  else if (b % 2 == 0) launch_pack<float, 2>(p, lam_face, chi_face, st);
+  else launch_pack<float, 1>(p, lam_face, chi_face, st);
   return check_launch("b200wd_halo_pack");
 }

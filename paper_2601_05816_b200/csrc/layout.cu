@@ -3,6 +3,7 @@
 // include/b200wd.h, plus the parity split/merge of oddeven.py:72-95.
 #include "capi.cuh"
 #include "common.cuh"
+#include "layout.cuh"
 
 namespace b200wd {
 
@@ -14,18 +15,26 @@ template <> __device__ __forceinline__ float2 from_c128<float2>(double2 v) {
 __device__ __forceinline__ double2 to_c128(double2 v) { return v; }
 __device__ __forceinline__ double2 to_c128(float2 v) { return make_double2(v.x, v.y); }
 
-// dst[(k*n + x)*b + r] <- src at the reference offset of (x, k, r)
+// device element i (site-blocked planes, layout.cuh) <-> reference offset
 template <typename C, bool IMPORT>
 __global__ void spinor_convert_kernel(const void* __restrict__ in, void* __restrict__ out, int layout, int64_t n,
                                       int s, int b) {
-  const int64_t total = n * s * b;
+  // device storage is padded to a whole number of 8-site blocks; padding
+  // sites are written as zeros on import and skipped on export
+  const int64_t total = ((n + 7) / 8) * 8 * s * b;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    // i enumerates the device planes: i = (k*n + x)*b + r
+    // i = (((blk * s + k) * 8 + lo) * b + r
     const int r = (int)(i % b);
-    const int64_t q = i / b;
-    const int64_t x = q % n;
-    const int k = (int)(q / n);
+    int64_t q = i / b;
+    const int lo = (int)(q & 7);
+    q >>= 3;
+    const int k = (int)(q % s);
+    const int64_t x = (q / s) * 8 + lo;
+    if (x >= n) {
+      if (IMPORT) static_cast<C*>(out)[i] = from_c128<C>(make_double2(0.0, 0.0));
+      continue;
+    }
     const int64_t ref = layout == 1 ? (x * b + r) * s + k : (x * s + k) * b + r;  // fields.py:53-64
     if (IMPORT) {
       static_cast<C*>(out)[i] = from_c128<C>(__ldg(static_cast<const double2*>(in) + ref));
@@ -35,30 +44,34 @@ __global__ void spinor_convert_kernel(const void* __restrict__ in, void* __restr
   }
 }
 
-// (n,4,3,3) row-major -> [mu][e][site]
+// (n,4,3,3) row-major -> site-blocked link planes
 template <typename C>
 __global__ void gauge_import_kernel(const double2* __restrict__ in, C* __restrict__ out, int64_t n) {
   const int64_t total = n * 36;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t x = i % n;
-    const int me = (int)(i / n);  // mu*9 + e
+    // i = (blk * 36 + me) * 8 + lo
+    const int lo = (int)(i & 7);
+    const int64_t q = i >> 3;
+    const int me = (int)(q % 36);  // mu*9 + e
+    const int64_t x = (q / 36) * 8 + lo;
     out[i] = from_c128<C>(__ldg(in + x * 36 + me));
   }
 }
 
-// full <-> parity planes; cb = site >> 1 (oddeven.py:62-65 ordering)
+// full <-> parity fields; cb = site >> 1 (oddeven.py:62-65 ordering)
 template <typename C, bool SPLIT>
 __global__ void parity_kernel(C* __restrict__ full, C* __restrict__ even, C* __restrict__ odd, int64_t n, int s,
                               int b, int X, int Y, int Z, int par0) {
   const int64_t total = n * s * b;
-  const int64_t nh = n / 2;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(i % b);
-    const int64_t q = i / b;
-    const int64_t site = q % n;
-    const int k = (int)(q / n);
+    int64_t q = i / b;
+    const int lo = (int)(q & 7);
+    q >>= 3;
+    const int k = (int)(q % s);
+    const int64_t site = (q / s) * 8 + lo;
     const int z = (int)(site % Z);
     int64_t c = site / Z;
     const int y = (int)(c % Y);
@@ -67,7 +80,7 @@ __global__ void parity_kernel(C* __restrict__ full, C* __restrict__ even, C* __r
     const int t = (int)(c / X);
     const int par = (t + x + y + z + par0) & 1;
     C* half = par ? odd : even;
-    const int64_t hi = ((int64_t)k * nh + (site >> 1)) * b + r;
+    const int64_t hi = spinor_elem(site >> 1, k, r, s, b);
     if (SPLIT) half[hi] = full[i];
     else full[i] = half[hi];
   }
@@ -89,7 +102,7 @@ extern "C" int b200wd_spinor_import(const void* src_c128, int32_t layout, int64_
   B200WD_REQUIRE(layout == 1 || layout == 2, "layout must be 1 (rhs-major) or 2 (component-major), got %d", layout);
   B200WD_REQUIRE(n_sites >= 1 && s >= 1 && b >= 1, "bad field shape n=%lld s=%d b=%d", (long long)n_sites, s, b);
   B200WD_REQUIRE(src_c128 && dst, "NULL pointer");
-  const int64_t total = n_sites * s * b;
+  const int64_t total = ((n_sites + 7) / 8) * 8 * s * b;
   if (dtype == B200WD_C128)
     spinor_convert_kernel<double2, true><<<grid_for(total), 256, 0, as_stream(stream)>>>(src_c128, dst, layout,
                                                                                           n_sites, s, b);
@@ -106,7 +119,7 @@ extern "C" int b200wd_spinor_export(const void* src, int32_t dtype, int64_t n_si
   B200WD_REQUIRE(layout == 1 || layout == 2, "layout must be 1 or 2, got %d", layout);
   B200WD_REQUIRE(n_sites >= 1 && s >= 1 && b >= 1, "bad field shape");
   B200WD_REQUIRE(src && dst_c128, "NULL pointer");
-  const int64_t total = n_sites * s * b;
+  const int64_t total = ((n_sites + 7) / 8) * 8 * s * b;
   if (dtype == B200WD_C128)
     spinor_convert_kernel<double2, false><<<grid_for(total), 256, 0, as_stream(stream)>>>(src, dst_c128, layout,
                                                                                            n_sites, s, b);
@@ -119,7 +132,8 @@ extern "C" int b200wd_spinor_export(const void* src, int32_t dtype, int64_t n_si
 }
 
 extern "C" int b200wd_gauge_import(const void* src_c128, int64_t n_sites, void* dst, int32_t dtype, void* stream) {
-  B200WD_REQUIRE(n_sites >= 1 && src_c128 && dst, "bad gauge import arguments");
+  B200WD_REQUIRE(n_sites >= 1 && n_sites % 8 == 0 && src_c128 && dst, "bad gauge import arguments (n=%lld)",
+                 (long long)n_sites);
   const int64_t total = n_sites * 36;
   if (dtype == B200WD_C128)
     gauge_import_kernel<double2><<<grid_for(total), 256, 0, as_stream(stream)>>>(

@@ -1,0 +1,199 @@
+// Device building blocks of the Wilson hopping term shared by the generic
+// (LDG) and the TMA-pipelined (cp.async.bulk -> smem) kernels.
+#pragma once
+#include "common.cuh"
+#include "layout.cuh"
+
+namespace b200wd {
+
+// A_mu blocks of the chiral basis as (permutation, unit phase code)
+// (projectors.py:40-48, 88-92).  Phase codes: 0:+1 1:+i 2:-1 3:-i.
+__host__ __device__ constexpr int a_perm(int mu, int s) { return (mu == 1 || mu == 2) ? 1 - s : s; }
+__host__ __device__ constexpr int a_code(int mu, int s) {
+  return mu == 0 ? 0 : mu == 1 ? 1 : mu == 2 ? (s == 0 ? 0 : 2) : (s == 0 ? 1 : 3);
+}
+// A_mu^H has the same permutation; its phases are the conjugates.
+__host__ __device__ constexpr int adj_code(int mu, int s) {
+  return mu == 0 ? 0 : mu == 1 ? 3 : mu == 2 ? (s == 0 ? 2 : 0) : (s == 0 ? 3 : 1);
+}
+
+struct HopParams {
+  int32_t T, X, Y, Z;
+  int32_t par0;        // parity of local slice 0 (t_origin & 1)
+  int32_t b;           // rhs count
+  int32_t dst_parity;  // -1: full lattice
+  int64_t n;           // local sites
+  int64_t n_src, n_dst;
+  int64_t d_begin, d_end;  // destination index range in the dst field
+  int64_t per_t;           // X*Y*Z
+  int64_t nf;              // face sites of the src field
+  const void* U;
+  const void* src;
+  const void* xself;
+  void* out;
+  double alpha, beta;  // beta carries the 1/2 of the projectors
+  const double* scale;
+  const void* lam_halo;
+  const void* chi_halo;
+};
+
+// ---- V-wide loads/stores of consecutive rhs ---------------------------------
+template <typename R, int V> struct VecIO;
+template <> struct VecIO<double, 1> {
+  static __device__ __forceinline__ void ld(double2 (&o)[1], const double2* p) { o[0] = __ldg(p); }
+  static __device__ __forceinline__ void lds(double2 (&o)[1], const double2* p) { o[0] = *p; }
+  static __device__ __forceinline__ void st(double2* p, const double2 (&v)[1]) { __stcs(p, v[0]); }
+};
+template <> struct VecIO<float, 1> {
+  static __device__ __forceinline__ void ld(float2 (&o)[1], const float2* p) { o[0] = __ldg(p); }
+  static __device__ __forceinline__ void lds(float2 (&o)[1], const float2* p) { o[0] = *p; }
+  static __device__ __forceinline__ void st(float2* p, const float2 (&v)[1]) { __stcs(p, v[0]); }
+};
+template <> struct VecIO<float, 2> {
+  static __device__ __forceinline__ void ld(float2 (&o)[2], const float2* p) {
+    float4 q = __ldg(reinterpret_cast<const float4*>(p));
+    o[0] = make_float2(q.x, q.y);
+    o[1] = make_float2(q.z, q.w);
+  }
+  static __device__ __forceinline__ void lds(float2 (&o)[2], const float2* p) {
+    float4 q = *reinterpret_cast<const float4*>(p);
+    o[0] = make_float2(q.x, q.y);
+    o[1] = make_float2(q.z, q.w);
+  }
+  static __device__ __forceinline__ void st(float2* p, const float2 (&v)[2]) {
+    __stcs(reinterpret_cast<float4*>(p), make_float4(v[0].x, v[0].y, v[1].x, v[1].y));
+  }
+};
+
+// g = M h for the two colour vectors, M = U (DAG=false) or U^H (DAG=true).
+template <bool DAG>
+__device__ __forceinline__ void matvec2(double2 (&g)[2][3], const double2 (&u)[9],
+                                        const double2 (&h)[2][3]) {
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      double2 a = mk(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) a = DAG ? cmacc(a, u[3 * j + i], h[s][j]) : cmac(a, u[3 * i + j], h[s][j]);
+      g[s][i] = a;
+    }
+}
+template <bool DAG>
+__device__ __forceinline__ void matvec2(float2 (&g)[2][3], const float2 (&u)[9], const float2 (&h)[2][3]) {
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    float2 hs[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) hs[j] = mk(-h[s][j].y, h[s][j].x);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      float2 a = mk(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        a = DAG ? cmacc_s(a, u[3 * j + i], h[s][j], hs[j]) : cmac_s(a, u[3 * i + j], h[s][j], hs[j]);
+      g[s][i] = a;
+    }
+  }
+}
+
+// h_s = u_s - sign * A_mu l_s without the 1/2 (projectors.py:126-136);
+// FWD is the sign -1 (lambda) projection, !FWD the sign +1 (chi) one.
+template <int MU, bool FWD, int S, typename C>
+__device__ __forceinline__ void project_spin(C (&h)[3], const C (&psi)[12]) {
+  constexpr int code = FWD ? a_code(MU, S) : ((a_code(MU, S) + 2) & 3);
+  constexpr int lp = 6 + 3 * a_perm(MU, S);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) h[c] = cadd(psi[3 * S + c], phase<code>(psi[lp + c]));
+}
+
+// acc += reconstruct(g) for sign -1 (FWD: lower += A^H g) or +1 (lower -= A^H g)
+// (projectors.py:144-147, dirac.py:258-263)
+template <int MU, bool FWD, int S, typename C>
+__device__ __forceinline__ void accumulate_spin(C (&acc)[12], const C (&g)[2][3]) {
+  constexpr int code = FWD ? adj_code(MU, S) : ((adj_code(MU, S) + 2) & 3);
+  constexpr int gp = a_perm(MU, S);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    acc[3 * S + c] = cadd(acc[3 * S + c], g[S][c]);
+    acc[6 + 3 * S + c] = cadd(acc[6 + 3 * S + c], phase<code>(g[gp][c]));
+  }
+}
+
+// One hop from a full neighbour spinor (12 components).  SS / SL: the
+// spinor / link pointer is in shared memory (plain loads -> LDS) rather than
+// global memory (read-only LDG).
+template <int MU, bool FWD, typename R, int V, bool SS = false, bool SL = false>
+__device__ __forceinline__ void hop_full(cx<R> (&acc)[V][12], const cx<R>* __restrict__ sp, int64_t kstride,
+                                         const cx<R>* __restrict__ up, int64_t estride) {
+  using C = cx<R>;
+  C psi[V][12];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    C tmp[V];
+    if constexpr (SS) VecIO<R, V>::lds(tmp, sp + k * kstride);
+    else VecIO<R, V>::ld(tmp, sp + k * kstride);
+#pragma unroll
+    for (int v = 0; v < V; ++v) psi[v][k] = tmp[v];
+  }
+  C u[9];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) u[e] = SL ? up[e * estride] : __ldg(up + e * estride);
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    C h[2][3], g[2][3];
+    project_spin<MU, FWD, 0>(h[0], psi[v]);
+    project_spin<MU, FWD, 1>(h[1], psi[v]);
+    matvec2<!FWD>(g, u, h);
+    accumulate_spin<MU, FWD, 0>(acc[v], g);
+    accumulate_spin<MU, FWD, 1>(acc[v], g);
+  }
+}
+
+// Forward T hop whose projected half spinor comes from the lam halo face.
+template <typename R, int V>
+__device__ __forceinline__ void hop_lam_halo(cx<R> (&acc)[V][12], const cx<R>* __restrict__ hp, int64_t hstride,
+                                             const cx<R>* __restrict__ up, int64_t estride) {
+  using C = cx<R>;
+  C hh[V][6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    C tmp[V];
+    VecIO<R, V>::ld(tmp, hp + k * hstride);
+#pragma unroll
+    for (int v = 0; v < V; ++v) hh[v][k] = tmp[v];
+  }
+  C u[9];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) u[e] = __ldg(up + e * estride);
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    C h[2][3], g[2][3];
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) h[s][c] = hh[v][3 * s + c];
+    matvec2<false>(g, u, h);
+    accumulate_spin<0, true, 0>(acc[v], g);
+    accumulate_spin<0, true, 1>(acc[v], g);
+  }
+}
+
+// Backward T hop whose U^H-multiplied half spinor comes from the chi face.
+template <typename R, int V>
+__device__ __forceinline__ void hop_chi_halo(cx<R> (&acc)[V][12], const cx<R>* __restrict__ hp, int64_t hstride) {
+  using C = cx<R>;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    C tmp[V];
+    VecIO<R, V>::ld(tmp, hp + k * hstride);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      // sign +1 reconstruction with A_0 = I: upper += g, lower -= g
+      acc[v][k] = cadd(acc[v][k], tmp[v]);
+      acc[v][6 + k] = csub(acc[v][6 + k], tmp[v]);
+    }
+  }
+}
+
+}  // namespace b200wd

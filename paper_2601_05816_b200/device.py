@@ -3,10 +3,11 @@
 PyTorch is used only as plumbing: CUDA memory (caching allocator), streams
 and pinned host buffers.  Every byte of compute goes through libb200wd.
 
-Device layouts (include/b200wd.h):
-  * spinor block field -> torch tensor of shape (s, n, b), complex128 or
-    complex64: "component planes", rhs innermost;
-  * links -> (4, 9, n): one plane per (direction, 3x3 entry).
+Device layouts (include/b200wd.h, csrc/layout.cuh):
+  * spinor block field -> torch tensor (n/8, s, 8, b), complex128 or
+    complex64: site-blocked component planes, rhs innermost;
+  * links -> (n/8, 36, 8): per 8-site block, one run of 8 per
+    (direction, 3x3 entry).
 The upload path copies the reference storage (Layout 1 or 2, complex128) as
 raw bytes and converts with a device kernel; the download path is the exact
 inverse.
@@ -59,30 +60,42 @@ def ptr(t) -> int | None:
     return None if t is None else int(t.data_ptr())
 
 
+SITE_BLOCK = 8
+
+
+def _blocks(n: int) -> int:
+    return -(-n // SITE_BLOCK)
+
+
 @dataclass
 class DeviceField:
-    """A block spinor field resident in HBM (component planes, rhs innermost).
+    """A block spinor field resident in HBM.
 
-    ``parity`` is None for a full-lattice field, 0/1 for a checkerboard
-    field whose site cb is the natural site ``2*cb + (0|1)`` of that parity.
+    Storage is the site-blocked component-plane layout of csrc/layout.cuh:
+    ``data`` has shape (ceil(n/8), s, 8, b), i.e. element (site, k, r) at
+    data[site // 8, k, site % 8, r]; rhs is innermost.  Fields whose site
+    count is not a multiple of 8 (only synthetic, non-lattice fields) carry
+    zero padding sites.  ``parity`` is None for a full-lattice field, 0/1 for
+    a checkerboard field whose site cb is the natural site 2*cb + (0|1).
     """
 
-    data: "torch.Tensor"  # (s, n, b)
+    data: "torch.Tensor"
+    n: int
     geom: LatticeGeometry | None = None
     parity: int | None = None
     layout: Layout = Layout.COMPONENT_MAJOR  # layout used when downloaded
 
     @property
     def s(self) -> int:
-        return int(self.data.shape[0])
-
-    @property
-    def n_sites(self) -> int:
         return int(self.data.shape[1])
 
     @property
+    def n_sites(self) -> int:
+        return self.n
+
+    @property
     def b(self) -> int:
-        return int(self.data.shape[2])
+        return int(self.data.shape[3])
 
     @property
     def dtype(self) -> str:
@@ -95,23 +108,37 @@ class DeviceField:
     @classmethod
     def zeros(cls, n_sites, b, s=SPINOR_LEN, dtype="c128", geom=None, parity=None, layout=Layout.COMPONENT_MAJOR):
         dev = require_device()
-        t = torch.zeros((s, n_sites, b), dtype=torch_dtype(dtype), device=dev)
-        return cls(t, geom, parity, Layout(layout))
+        t = torch.zeros((_blocks(n_sites), s, SITE_BLOCK, b), dtype=torch_dtype(dtype), device=dev)
+        return cls(t, int(n_sites), geom, parity, Layout(layout))
 
     @classmethod
     def empty(cls, n_sites, b, s=SPINOR_LEN, dtype="c128", geom=None, parity=None, layout=Layout.COMPONENT_MAJOR):
+        if n_sites % SITE_BLOCK:
+            return cls.zeros(n_sites, b, s, dtype, geom, parity, layout)  # padding must read as zero
         dev = require_device()
-        t = torch.empty((s, n_sites, b), dtype=torch_dtype(dtype), device=dev)
-        return cls(t, geom, parity, Layout(layout))
+        t = torch.empty((_blocks(n_sites), s, SITE_BLOCK, b), dtype=torch_dtype(dtype), device=dev)
+        return cls(t, int(n_sites), geom, parity, Layout(layout))
+
+    @classmethod
+    def from_logical(cls, logical: "torch.Tensor", geom=None, parity=None) -> "DeviceField":
+        """(n, s, b) device tensor in logical order -> DeviceField (tests, benches)."""
+        n, s, b = logical.shape
+        nb = _blocks(n)
+        if nb * SITE_BLOCK != n:
+            pad = torch.zeros((nb * SITE_BLOCK - n, s, b), dtype=logical.dtype, device=logical.device)
+            logical = torch.cat([logical, pad])
+        data = logical.reshape(nb, SITE_BLOCK, s, b).permute(0, 2, 1, 3).contiguous()
+        return cls(data, int(n), geom, parity)
 
     def empty_like(self) -> "DeviceField":
-        return DeviceField(torch.empty_like(self.data), self.geom, self.parity, self.layout)
+        alloc = torch.zeros_like if self.n % SITE_BLOCK else torch.empty_like
+        return DeviceField(alloc(self.data), self.n, self.geom, self.parity, self.layout)
 
     def zeros_like(self) -> "DeviceField":
-        return DeviceField(torch.zeros_like(self.data), self.geom, self.parity, self.layout)
+        return DeviceField(torch.zeros_like(self.data), self.n, self.geom, self.parity, self.layout)
 
     def copy(self) -> "DeviceField":
-        return DeviceField(self.data.clone(), self.geom, self.parity, self.layout)
+        return DeviceField(self.data.clone(), self.n, self.geom, self.parity, self.layout)
 
     @property
     def ptr(self) -> int:
@@ -121,9 +148,14 @@ class DeviceField:
         """Download into the reference storage order (complex128)."""
         return download(self, layout, out)
 
+    def logical_tensor(self) -> "torch.Tensor":
+        """(n, s, b) device view in logical [site, component, rhs] order (copy)."""
+        nb = self.data.shape[0]
+        return self.data.permute(0, 2, 1, 3).reshape(nb * SITE_BLOCK, self.s, self.b)[: self.n]
+
     def logical(self) -> np.ndarray:
         """(n, s, b) complex128 numpy copy (tests / diagnostics)."""
-        return self.data.permute(1, 0, 2).to(torch.complex128).cpu().numpy()
+        return self.logical_tensor().to(torch.complex128).cpu().numpy()
 
 
 def _host_array(field) -> np.ndarray:
@@ -141,7 +173,7 @@ def upload(field, dtype: str = "c128", stream=None, parity=None) -> DeviceField:
     if isinstance(field, DeviceField):
         if field.dtype == dtype:
             return field
-        return DeviceField(field.data.to(torch_dtype(dtype)), field.geom, field.parity, field.layout)
+        return DeviceField(field.data.to(torch_dtype(dtype)), field.n, field.geom, field.parity, field.layout)
     dev = require_device()
     arr = _host_array(field)
     raw = torch.from_numpy(arr).to(dev, non_blocking=True)
@@ -172,7 +204,7 @@ def download(df: DeviceField, layout=None, out: BlockSpinorField | None = None, 
 
 @dataclass
 class DeviceGauge:
-    """Links resident in HBM as (4, 9, n) planes of one dtype."""
+    """Links resident in HBM as (n/8, 36, 8) site-blocked planes of one dtype."""
 
     data: "torch.Tensor"
     geom: LatticeGeometry
@@ -193,7 +225,7 @@ def upload_gauge(gauge, dtype: str = "c128", stream=None) -> DeviceGauge:
     if data.shape != (n, 4, 3, 3):
         raise ValueError(f"gauge data has shape {data.shape}, expected {(n, 4, 3, 3)}")
     raw = torch.from_numpy(data.reshape(-1)).to(dev, non_blocking=True)
-    out = torch.empty((4, 9, n), dtype=torch_dtype(dtype), device=dev)
+    out = torch.empty((n // SITE_BLOCK, 36, SITE_BLOCK), dtype=torch_dtype(dtype), device=dev)
     _lib.call("b200wd_gauge_import", ptr(raw), n, ptr(out), dtype_code(dtype), stream_ptr(stream))
     return DeviceGauge(out, gauge.geom)
 

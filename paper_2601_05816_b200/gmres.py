@@ -108,7 +108,7 @@ class _HostOp:
     def apply_device(self, v: DeviceField, out=None, scale=None):
         res = upload(self.fn(v.to_host(self.layout)), v.dtype)
         if scale is not None:
-            res.data.mul_(scale.to(res.data.dtype)[None, None, :])
+            res.data.mul_(scale.to(res.data.dtype)[None, None, None, :])
         if out is None:
             return res
         out.data.copy_(res.data)
@@ -125,13 +125,12 @@ class MatrixOp:
         self.allreduce = None
 
     def apply_device(self, v: DeviceField, out=None, scale=None):
-        s, n, b = v.data.shape
-        cols = v.data.permute(1, 0, 2).reshape(n * s, b)
-        res = (self.a @ cols).reshape(n, s, b).permute(1, 0, 2)
+        cols = v.logical_tensor().reshape(v.n_sites * v.s, v.b)
+        res = (self.a @ cols).reshape(v.n_sites, v.s, v.b)
         if scale is not None:
             res = res * scale.to(res.dtype)[None, None, :]
         out = v.empty_like() if out is None else out
-        out.data.copy_(res)
+        out.data.copy_(DeviceField.from_logical(res).data)
         return out
 
     def __call__(self, v):

@@ -186,7 +186,8 @@ def test_tsplit_halo_kernels_reproduce_single_gpu(nranks, parity):
         lg = P.LatticeGeometry((tl,) + dims[1:])
         lat = _lib.Lattice.make(lg.dims, r * tl)
         gl = upload_gauge(P.GaugeField(lg, links[r * tl * per_t:(r + 1) * tl * per_t]))
-        src = DeviceField(src_full.data[:, r * tl * per:(r + 1) * tl * per].contiguous())
+        nloc = tl * per
+        src = DeviceField(src_full.data[r * nloc // 8:(r + 1) * nloc // 8].contiguous(), nloc)
         lam = torch.empty((6, per, 3), dtype=torch.complex128, device="cuda")
         chi = torch.empty_like(lam)
         sp = -1 if parity is None else 1 - parity
@@ -196,7 +197,7 @@ def test_tsplit_halo_kernels_reproduce_single_gpu(nranks, parity):
     for r, (lg, lat, gl, src, _, _) in enumerate(slabs):
         lam_from_up = slabs[(r + 1) % nranks][4]
         chi_from_down = slabs[(r - 1) % nranks][5]
-        out = DeviceField(torch.empty_like(src.data))
+        out = DeviceField(torch.empty_like(src.data), src.n)
         if parity is None:
             hop_device(lat, "c128", 3, -1, gl, src, out, src, 4.1, -1.0, lam_halo=lam_from_up,
                        chi_halo=chi_from_down)
@@ -204,6 +205,6 @@ def test_tsplit_halo_kernels_reproduce_single_gpu(nranks, parity):
             hop_device(lat, "c128", 3, parity, gl, src, out, None, 0.0, 1.0, lam_halo=lam_from_up,
                        chi_halo=chi_from_down)
         outs.append(out.data)
-    got = torch.cat(outs, dim=1)
+    got = torch.cat(outs, dim=0)
     err = (got - ref.data).abs().max().item() / ref.data.abs().max().item()
     assert err < 1e-14

@@ -25,8 +25,8 @@ geom = P.LatticeGeometry(tuple(a.dims))
 gauge = upload_gauge(P.gen_gauge(geom, "random", seed=0), a.dtype)
 n = geom.n_sites if a.parity < 0 else geom.n_sites // 2
 tdt = torch.complex128 if a.dtype == "c128" else torch.complex64
-psi = DeviceField(torch.randn((12, n, a.b), dtype=torch.complex128, device="cuda").to(tdt))
-eta = DeviceField(torch.empty_like(psi.data))
+psi = DeviceField(torch.randn((n // 8, 12, 8, a.b), dtype=torch.complex128, device="cuda").to(tdt), n)
+eta = DeviceField(torch.empty_like(psi.data), n)
 lat = _lib.Lattice.make(geom.dims)
 code = 0 if a.dtype == "c128" else 1
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
