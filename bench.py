@@ -40,6 +40,19 @@ M0 = 0.1
 METRIC = "D_W apply site*rhs/s (16^3x32, nrhs=16, c128)"
 
 
+PROFILE = ROOT / "profiles" / "r1_ncu_ring_c128_b16_cfg2.json"
+
+
+def profile_traffic():
+    """DRAM bytes per launch of the headline kernel from the committed ncu
+    --set full capture (profiles/), or None."""
+    try:
+        d = json.loads(PROFILE.read_text())
+        return d["launches"][0]["dram_traffic_bytes"]
+    except Exception:
+        return None
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -204,25 +217,63 @@ def gpu_gmres(args, torch, P):
     return out
 
 
-def cpu_baseline_sample(b=16, reps=3):
-    """Oracle port (numpy restatement of lqcdlab) on a 16^3 x 2 slab sample."""
+def _slab_worker(args):
+    """One T slab of the sample lattice (oracle restatement, halo.py semantics)."""
+    from oracle import lqcd_oracle as O
+    r, nr = args
+    links, psi, dims = _SAMPLE["links"], _SAMPLE["psi"], _SAMPLE["dims"]
+    tl = dims[0] // nr
+    per_t = dims[1] * dims[2] * dims[3]
+    sl = slice(r * tl * per_t, (r + 1) * tl * per_t)
+    up = slice(((r + 1) % nr) * tl * per_t, ((r + 1) % nr) * tl * per_t + tl * per_t)
+    dn = slice(((r - 1) % nr) * tl * per_t, ((r - 1) % nr) * tl * per_t + tl * per_t)
+    lam_up, _ = O.tsplit_faces(links[up], psi[up], per_t)
+    _, chi_dn = O.tsplit_faces(links[dn], psi[dn], per_t)
+    out = O.tsplit_local_apply((tl,) + tuple(dims[1:]), M0, links[sl], psi[sl], lam_up, chi_dn)
+    return float(np.abs(out[:4]).sum())
+
+
+_SAMPLE: dict = {}
+
+
+def cpu_apply_rate(cores: int, steps: int, warmup: int, b: int = 16):
+    """Oracle port of lqcdlab.apply_dirac on the host cores: a sample lattice
+    of 16^3 x (2*cores) sites split in T slabs, one slab (2 slices, 8192
+    sites) per worker process, numpy's threadpools pinned to 1 thread each.
+    Returns (site*rhs/s, seconds per step, sample description)."""
+    import multiprocessing as mp
+
     from threadpoolctl import threadpool_limits
 
     from oracle import lqcd_oracle as O
-    dims = (2, 16, 16, 16)
-    n = 2 * 16 ** 3
-    links = O.gen_gauge_random(dims, 0)
-    psi = O.gen_spinor(n, b, 2)
+    dims = (2 * cores, 16, 16, 16)
+    n = dims[0] * 16 ** 3
+    _SAMPLE.update(dims=dims, links=O.gen_gauge_random(dims, 0), psi=O.gen_spinor(n, b, 2))
     with threadpool_limits(1):
-        O.apply_dirac(dims, M0, links, None, psi)
+        if cores == 1:
+            run = lambda: _slab_worker((0, 1))  # noqa: E731
+            pool = None
+        else:
+            pool = mp.get_context("fork").Pool(cores)
+            run = lambda: pool.map(_slab_worker, [(r, cores) for r in range(cores)])  # noqa: E731
+        for _ in range(warmup):
+            run()
         ts = []
-        for _ in range(reps):
+        for _ in range(steps):
             t0 = time.perf_counter()
-            O.apply_dirac(dims, M0, links, None, psi)
+            run()
             ts.append(time.perf_counter() - t0)
+        if pool is not None:
+            pool.close()
     t = float(np.median(ts))
-    return {"value": n * b / t, "unit": "site*rhs/s", "cores": 1, "kind": "port",
-            "sample": f"oracle apply_dirac on a 16^3x2 slab (8192 sites), nrhs={b}, c128, median of {reps}"}
+    sample = (f"oracle apply_dirac (numpy port of lqcdlab dirac.py) on a 16^3x{dims[0]} sample lattice, "
+              f"nrhs={b}, c128, {cores} worker process(es) x 8192 sites, median of {steps} steps")
+    return n * b / t, t, sample
+
+
+def cpu_baseline_sample(b=16, reps=3):
+    v, t, sample = cpu_apply_rate(1, reps, 1, b)
+    return {"value": v, "unit": "site*rhs/s", "cores": 1, "kind": "port", "sample": sample}
 
 
 def main():
@@ -254,8 +305,9 @@ def main():
                    "lattice": list(CFG2_DIMS), "nrhs": 16, "m0": M0, "l2": "rotating buffers > 4x L2 between reuses",
                    "parallelism": "single GPU"},
         "roofline": {"bound": "hbm", "achieved": head["hbm_gbs"], "peak": hbm_peak, "unit": "GB/s",
-                     "frac": head["frac"], "traffic": None, "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_launch": head["bytes_per_launch"]},
+                     "frac": head["frac"], "traffic": profile_traffic(), "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": head["bytes_per_launch"],
+                     "kernel": "hop_ring_kernel<double,1,16> (libb200wd.so, b200wd_dirac_apply)"},
         "e2e": e2e, "gpu_launches": args.steps, "clocks": clk,
         "sweep": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()} for r in sweep],
     }
@@ -270,32 +322,16 @@ def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    b = HEADLINE[1]
-    from threadpoolctl import threadpool_limits
-
-    from oracle import lqcd_oracle as O
-    dims = (2, 16, 16, 16)
-    n = 2 * 16 ** 3
-    links = O.gen_gauge_random(dims, 0)
-    psi = O.gen_spinor(n, b, 2)
-    cores = os.cpu_count() or 1
-    with threadpool_limits(cores):
-        for _ in range(args.warmup):
-            O.apply_dirac(dims, M0, links, None, psi)
-        ts = []
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            O.apply_dirac(dims, M0, links, None, psi)
-            ts.append(time.perf_counter() - t0)
-    t = float(np.mean(ts))
-    v = n * b / t
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    steps = max(1, min(args.steps, 10))
+    v, t, sample = cpu_apply_rate(cores, steps, min(args.warmup, 2), HEADLINE[1])
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "site*rhs/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": "BASELINE configs[1] sample: 16^3x2 slab of the 16^3x32 lattice, nrhs=16, c128",
-                       "lattice": [2, 16, 16, 16], "nrhs": b, "m0": M0},
-            "cpu_baseline": {"value": v, "unit": "site*rhs/s", "cores": cores, "kind": "port",
-                             "sample": "oracle (numpy port of lqcdlab apply_dirac) on a 16^3x2 slab, 8192 sites"},
+            "steps": steps, "warmup": min(args.warmup, 2), "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded SU(3) links, Gaussian rhs)",
+            "config": {"workload": "BASELINE configs[1] sample: D_W apply, nrhs=16, c128, 16^3 spatial volume, "
+                                   f"T = 2 x {cores} slab sample", "lattice": [2 * cores, 16, 16, 16],
+                       "nrhs": HEADLINE[1], "m0": M0},
+            "cpu_baseline": {"value": v, "unit": "site*rhs/s", "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "site*rhs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 

@@ -164,8 +164,13 @@ template <typename R, int V, int B> struct RingShape {
   static constexpr int SPIN = NB * 96 * B;                           // complex per spinor tile
   static constexpr int SLOT = SPIN + NB * 72;                        // + one link plane per block
   static constexpr int SLOT_BYTES = SLOT * (int)sizeof(cx<R>);
-  static constexpr int S = SLOT_BYTES <= 28 * 1024 ? 3 : 2;          // hop-ring depth
-  static constexpr size_t SMEM = (size_t)SLOT_BYTES * (S + 1) + 8 * 2 * (S + 1);
+#ifndef B200WD_RING_BYTES
+#define B200WD_RING_BYTES (104 * 1024)
+#endif
+  static constexpr int S0 = B200WD_RING_BYTES / SLOT_BYTES;
+  static constexpr int S = S0 < 2 ? 2 : (S0 > 7 ? 7 : S0);          // ring depth (<= 7 tiles per item)
+  static constexpr int EDGE = 2 * NB * 12 * B;  // z-edge sites of the own blocks (one buffer: see producer)
+  static constexpr size_t SMEM = (size_t)SLOT_BYTES * S + EDGE * sizeof(cx<R>) + 8 * 2 * S;
 };
 
 // Coordinates of the first site of a site block (32-bit arithmetic: a rank's
@@ -213,16 +218,62 @@ __device__ __forceinline__ int64_t block_neighbor(int64_t g, const BlkCoord& c, 
   return ns >> 3;
 }
 
+// z neighbour (step +1 / -1 along z) of site d of a line with extent Z
+__device__ __forceinline__ int64_t z_neighbor(int64_t d, int z, int Z, int step) {
+  if (step > 0) return (z + 1 == Z) ? d - (Z - 1) : d + 1;
+  return (z == 0) ? d + (Z - 1) : d - 1;
+}
+
 // tile H in 0..5: hop (mu = H/2, forward if H even); H == 6: own block (z tile)
+// plus the z-edge sites outside the item (into `edge`)
 template <typename R, int V, int B, int H>
 __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, BlkCoord c, cx<R>* slot,
-                                           uint64_t* full) {
+                                           uint64_t* full, cx<R>* edge) {
   using C = cx<R>;
   using Sh = RingShape<R, V, B>;
-  constexpr uint32_t bytes = (uint32_t)(Sh::SLOT * sizeof(C));
-  mbar_expect_tx(full, bytes);
   const C* src = static_cast<const C*>(p.src);
   const C* U = static_cast<const C*>(p.U);
+  uint32_t bytes = (uint32_t)(Sh::SLOT * sizeof(C));
+  if constexpr (H == 6) {
+    // z-edge sites: site lo=0's z-1 and lo=7's z+1 neighbour of every block,
+    // when they fall outside the item's blocks (12 runs of B complex each)
+    BlkCoord ce = c;
+    uint32_t extra = 0;
+#pragma unroll 1
+    for (int jj = 0; jj < Sh::NB; ++jj) {
+      const int64_t g = gb0 + jj;
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int64_t dd = g * 8 + (side ? 7 : 0);
+        const int64_t nd = z_neighbor(dd, ce.z0 + (side ? 7 : 0), p.Z, side ? 1 : -1);
+        const int64_t jb = (nd >> 3) - gb0;
+        if (jb < 0 || jb >= Sh::NB) extra += 12 * B * sizeof(C);
+      }
+      if (jj + 1 < Sh::NB) block_step(ce, p);
+    }
+    bytes += extra;
+  }
+  mbar_expect_tx(full, bytes);
+  if constexpr (H == 6) {
+    BlkCoord ce = c;
+#pragma unroll 1
+    for (int jj = 0; jj < Sh::NB; ++jj) {
+      const int64_t g = gb0 + jj;
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int64_t dd = g * 8 + (side ? 7 : 0);
+        const int64_t nd = z_neighbor(dd, ce.z0 + (side ? 7 : 0), p.Z, side ? 1 : -1);
+        const int64_t jb = (nd >> 3) - gb0;
+        if (jb < 0 || jb >= Sh::NB) {
+          const C* es = src + spinor_base(nd, 12, B);
+          C* ed = edge + (jj * 2 + side) * 12 * B;
+#pragma unroll 1
+          for (int k = 0; k < 12; ++k) bulk_g2s(ed + k * B, es + k * 8 * B, B * sizeof(C), full);
+        }
+      }
+      if (jj + 1 < Sh::NB) block_step(ce, p);
+    }
+  }
 #pragma unroll
   for (int jj = 0; jj < Sh::NB; ++jj) {
     const int64_t g = gb0 + jj;
@@ -249,15 +300,16 @@ __global__ void __launch_bounds__(RingShape<R, V, B>::NT) hop_ring_kernel(const 
   constexpr int KST = 8 * B;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   C* ring = reinterpret_cast<C*>(smem_raw);
-  C* zbuf = ring + S * Sh::SLOT;
-  uint64_t* full = reinterpret_cast<uint64_t*>(zbuf + Sh::SLOT);  // [S] ring + [1] z
-  uint64_t* empty = full + (S + 1);
+  C* edge = ring + S * Sh::SLOT;  // single buffer: item i's z tile is issued only after
+                                  // item i-1's z tile was consumed (S <= 7 tiles per item)
+  uint64_t* full = reinterpret_cast<uint64_t*>(edge + Sh::EDGE);
+  uint64_t* empty = full + S;
 
   const int tid = threadIdx.x;  // 1-D block: consumers [0, NC), producer warp [NC, NC+32)
   const bool producer = tid >= Sh::NC;
   if (tid == 0) {
 #pragma unroll
-    for (int i = 0; i <= S; ++i) {
+    for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], Sh::NCW);
     }
@@ -267,17 +319,34 @@ __global__ void __launch_bounds__(RingShape<R, V, B>::NT) hop_ring_kernel(const 
 
   if (producer) {
     if (tid == Sh::NC) {  // one elected lane issues every copy
-      int seq = 0, zuse = 0;
+      int seq = 0;
+      const C* srcp = static_cast<const C*>(p.src);
+      const C* Up = static_cast<const C*>(p.U);
       for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int64_t gb0 = (p.d_begin >> 3) + it * Sh::NB;
         const BlkCoord c0 = block_coord(gb0, p);
+        // warm L2 with the compulsory misses of the next item of this CTA: its
+        // t+1 neighbour blocks and its own link blocks (first touch in sweep order)
+        const int64_t nx = it + gridDim.x;
+        if (nx < n_items) {
+          const int64_t gn = (p.d_begin >> 3) + nx * Sh::NB;
+          BlkCoord cn = block_coord(gn, p);
+#pragma unroll 1
+          for (int jj = 0; jj < Sh::NB; ++jj) {
+            const int64_t nb = block_neighbor<0, true>(gn + jj, cn, p);
+            bulk_prefetch_l2(srcp + nb * 96 * B, 96 * B * sizeof(C));
+            if (jj + 1 < Sh::NB) block_step(cn, p);
+          }
+          bulk_prefetch_l2(Up + gn * 288, Sh::NB * 288 * sizeof(C));
+        }
 #define B200WD_PRODUCE(H)                                                                 \
   {                                                                                       \
     const int slot = seq % S, use = seq / S;                                              \
     if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);                                  \
-    ring_issue<R, V, B, H>(p, gb0, c0, ring + slot * Sh::SLOT, &full[slot]);              \
+    ring_issue<R, V, B, H>(p, gb0, c0, ring + slot * Sh::SLOT, &full[slot], edge);        \
     ++seq;                                                                                \
   }
+        B200WD_PRODUCE(6)
         B200WD_PRODUCE(0)
         B200WD_PRODUCE(1)
         B200WD_PRODUCE(2)
@@ -285,9 +354,6 @@ __global__ void __launch_bounds__(RingShape<R, V, B>::NT) hop_ring_kernel(const 
         B200WD_PRODUCE(4)
         B200WD_PRODUCE(5)
 #undef B200WD_PRODUCE
-        if (zuse > 0) mbar_wait(&empty[S], (zuse - 1) & 1);
-        ring_issue<R, V, B, 6>(p, gb0, c0, zbuf, &full[S]);
-        ++zuse;
       }
     }
     return;
@@ -307,15 +373,69 @@ __global__ void __launch_bounds__(RingShape<R, V, B>::NT) hop_ring_kernel(const 
   const R beta = R(p.beta), alpha = R(p.alpha);
   const bool self_is_src = p.xself == p.src;
 
-  int seq = 0, zuse = 0;
+  // acc accumulates (alpha/beta) xself + 2H src, so out = (sc beta) acc: the own
+  // block (z tile) is consumed first and its slot recycled immediately
+  const R ab = (p.xself != nullptr && p.beta != 0.0) ? R(p.alpha / p.beta) : R(0);
+  R scb[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) scb[v] = sc[v] * beta;
+  int seq = 0;
   for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
     const int64_t gb0 = (p.d_begin >> 3) + it * Sh::NB;
     const int64_t d = (gb0 + j) * 8 + lo;
     C acc[V][12];
+    {
+      const int slot = seq % S;
+      mbar_wait(&full[slot], (seq / S) & 1);
+      const C* zt = ring + slot * Sh::SLOT;
+      // init from xself
+      if (self_is_src) {
 #pragma unroll
-    for (int v = 0; v < V; ++v)
+        for (int k = 0; k < 12; ++k) {
+          C xv[V];
+          VecIO<R, V>::lds(xv, zt + j * 96 * B + lo * B + r0 + k * KST);
 #pragma unroll
-      for (int k = 0; k < 12; ++k) acc[v][k] = mk(R(0), R(0));
+          for (int v = 0; v < V; ++v) acc[v][k] = mk(ab * xv[v].x, ab * xv[v].y);
+        }
+      } else if (p.xself) {
+        const C* xs = static_cast<const C*>(p.xself) + spinor_base(d, 12, B) + r0;
+#pragma unroll
+        for (int k = 0; k < 12; ++k) {
+          C xv[V];
+          VecIO<R, V>::ld(xv, xs + k * KST);
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[v][k] = mk(ab * xv[v].x, ab * xv[v].y);
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+#pragma unroll
+          for (int k = 0; k < 12; ++k) acc[v][k] = mk(R(0), R(0));
+      }
+      // z hops from the own blocks; z-edge sites from the edge buffer
+      const int z = (int)((uint32_t)d % (uint32_t)Z);
+      {
+        const int64_t nd = z_neighbor(d, z, Z, 1);
+        const int64_t jb = (nd >> 3) - gb0;
+        const bool in = jb >= 0 && jb < Sh::NB;
+        const C* sp = in ? zt + jb * 96 * B + (nd & 7) * B + r0 : edge + (j * 2 + 1) * 12 * B + r0;
+        const int kst = in ? KST : B;
+        hop_full<3, true, R, V, true, true>(acc, sp, kst, zt + Sh::SPIN + j * 72 + lo, 8);
+      }
+      {
+        const int64_t nd = z_neighbor(d, z, Z, -1);
+        const int64_t jb = (nd >> 3) - gb0;
+        const bool in = jb >= 0 && jb < Sh::NB;
+        const C* sp = in ? zt + jb * 96 * B + (nd & 7) * B + r0 : edge + (j * 2 + 0) * 12 * B + r0;
+        const int kst = in ? KST : B;
+        // U_3(x - z): own link plane, or global for an edge site (generic load)
+        const C* ul = in ? zt + Sh::SPIN + jb * 72 + (nd & 7) : U + link_base(nd) + 3 * 72;
+        hop_full<3, false, R, V, true, false, true>(acc, sp, kst, ul, 8);
+      }
+      __syncwarp();
+      if (lead) mbar_arrive(&empty[slot]);
+      ++seq;
+    }
 
 #define B200WD_CONSUME(H)                                                                            \
   {                                                                                                  \
@@ -336,52 +456,15 @@ __global__ void __launch_bounds__(RingShape<R, V, B>::NT) hop_ring_kernel(const 
     B200WD_CONSUME(5)
 #undef B200WD_CONSUME
 
-    // z hops from the own block; edge sites of a z line come from global memory
-    mbar_wait(&full[S], zuse & 1);
-    const int z = (int)((uint32_t)d % (uint32_t)Z);
-    {
-      const int64_t nd = (z + 1 == Z) ? d - (Z - 1) : d + 1;
-      const int64_t jb = (nd >> 3) - gb0;
-      const C* ul = zbuf + Sh::SPIN + j * 72 + lo;  // U_3(x) of the own block
-      if (jb >= 0 && jb < Sh::NB)
-        hop_full<3, true, R, V, true, true>(acc, zbuf + jb * 96 * B + (nd & 7) * B + r0, KST, ul, 8);
-      else
-        hop_full<3, true, R, V, false, true>(acc, src + spinor_base(nd, 12, B) + r0, KST, ul, 8);
-    }
-    {
-      const int64_t nd = (z == 0) ? d + (Z - 1) : d - 1;
-      const int64_t jb = (nd >> 3) - gb0;
-      if (jb >= 0 && jb < Sh::NB)
-        hop_full<3, false, R, V, true, true>(acc, zbuf + jb * 96 * B + (nd & 7) * B + r0, KST,
-                                             zbuf + Sh::SPIN + jb * 72 + (nd & 7), 8);
-      else
-        hop_full<3, false, R, V, false, false>(acc, src + spinor_base(nd, 12, B) + r0, KST,
-                                               U + link_base(nd) + 3 * 72, 8);
-    }
-    // epilogue: out = scale_r (alpha xself + beta acc)
-    const int64_t o = spinor_base(d, 12, B) + r0;
-    C* out = static_cast<C*>(p.out) + o;
-    const C* xs = p.xself ? static_cast<const C*>(p.xself) + o : nullptr;
-    const C* xz = zbuf + j * 96 * B + lo * B + r0;
+    // epilogue: out = sc beta acc = sc (alpha xself + beta 2H src / 2)
+    C* out = static_cast<C*>(p.out) + spinor_base(d, 12, B) + r0;
 #pragma unroll
     for (int k = 0; k < 12; ++k) {
       C res[V];
-      if (xs) {
-        C xv[V];
-        if (self_is_src) VecIO<R, V>::lds(xv, xz + k * KST);
-        else VecIO<R, V>::ld(xv, xs + k * KST);
 #pragma unroll
-        for (int v = 0; v < V; ++v)
-          res[v] = mk(sc[v] * (alpha * xv[v].x + beta * acc[v][k].x), sc[v] * (alpha * xv[v].y + beta * acc[v][k].y));
-      } else {
-#pragma unroll
-        for (int v = 0; v < V; ++v) res[v] = mk(sc[v] * beta * acc[v][k].x, sc[v] * beta * acc[v][k].y);
-      }
+      for (int v = 0; v < V; ++v) res[v] = mk(scb[v] * acc[v][k].x, scb[v] * acc[v][k].y);
       VecIO<R, V>::st(out + k * KST, res);
     }
-    __syncwarp();
-    if (lead) mbar_arrive(&empty[S]);
-    ++zuse;
   }
 }
 
@@ -392,7 +475,7 @@ static int g_sm_count = 0;
 template <typename R, int V, int B>
 static bool try_launch_ring(const HopParams& p, cudaStream_t st) {
   using Sh = RingShape<R, V, B>;
-  if (Sh::NC % 32 != 0) return false;
+  if (Sh::NC % 32 != 0 || p.beta == 0.0) return false;
   if (p.dst_parity >= 0 || p.lam_halo != nullptr || p.Z % 8 != 0) return false;
   if ((p.d_begin & 7) || (p.d_end & 7)) return false;
   const int64_t nblk = (p.d_end - p.d_begin) >> 3;

@@ -123,7 +123,7 @@ __device__ __forceinline__ void accumulate_spin(C (&acc)[12], const C (&g)[2][3]
 // One hop from a full neighbour spinor (12 components).  SS / SL: the
 // spinor / link pointer is in shared memory (plain loads -> LDS) rather than
 // global memory (read-only LDG).
-template <int MU, bool FWD, typename R, int V, bool SS = false, bool SL = false>
+template <int MU, bool FWD, typename R, int V, bool SS = false, bool SL = false, bool GL = false>
 __device__ __forceinline__ void hop_full(cx<R> (&acc)[V][12], const cx<R>* __restrict__ sp, int64_t kstride,
                                          const cx<R>* __restrict__ up, int64_t estride) {
   using C = cx<R>;
@@ -138,7 +138,10 @@ __device__ __forceinline__ void hop_full(cx<R> (&acc)[V][12], const cx<R>* __res
   }
   C u[9];
 #pragma unroll
-  for (int e = 0; e < 9; ++e) u[e] = SL ? up[e * estride] : __ldg(up + e * estride);
+  for (int e = 0; e < 9; ++e) {
+    if constexpr (GL) u[e] = up[e * estride];  // generic pointer: shared or global
+    else u[e] = SL ? up[e * estride] : __ldg(up + e * estride);
+  }
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     C h[2][3], g[2][3];
