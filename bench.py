@@ -276,6 +276,73 @@ def cpu_baseline_sample(b=16, reps=3):
     return {"value": v, "unit": "site*rhs/s", "cores": 1, "kind": "port", "sample": sample}
 
 
+def multi_gpu(args, torch, P):
+    """N ranks under torchrun: weak scaling of configs[1] over a T split.
+
+    Every rank owns a 16^3 x 32 slab (the N=1 workload) of a 16^3 x 32N
+    lattice; each step is one split D_W apply (face pack, NCCL send/recv
+    overlapped with the interior slices, boundary slices with halos).
+    value = all ranks' site*rhs / max-over-ranks device time.
+    """
+    import torch.distributed as dist
+
+    from paper_2601_05816_b200.device import DeviceField
+    from paper_2601_05816_b200.dirac import compulsory_bytes_per_site
+    from paper_2601_05816_b200.tsplit import TSplitComm
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    dt, b = HEADLINE
+    gdims = (CFG2_DIMS[0] * world,) + CFG2_DIMS[1:]
+    ggeom = P.LatticeGeometry(gdims)
+    comm = TSplitComm(ggeom)
+    lg, t0 = comm.local_geom, comm.t_origin
+    links = P.near_unit_links(gdims, 0.3, 0, t0, t0 + lg.dims[0])
+    gauge = P.flip_time_boundary(P.GaugeField(lg, links), gdims[0], t0)
+    comm.bind(P.DiracParams(m0=M0), gauge, None, dt)
+    n = lg.n_sites
+    nbuf = 2
+    g = torch.Generator(device="cpu").manual_seed(rank)
+    psis = [DeviceField(torch.randn((n // 8, 12, 8, b), dtype=torch.complex128, generator=g).to(dev), n)
+            for _ in range(nbuf)]
+    etas = [DeviceField(torch.empty_like(psis[0].data), n) for _ in range(nbuf)]
+    stream = torch.cuda.current_stream()
+    for i in range(args.warmup):
+        comm.apply_device(psis[i % nbuf], etas[i % nbuf])
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = ClockSampler(dev.index).start() if rank == 0 else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        comm.apply_device(psis[i % nbuf], etas[i % nbuf])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1) * 1e-3 / args.steps], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    clk = clocks.stop() if clocks else None
+    tt = float(t.item())
+    if rank == 0:
+        alg = compulsory_bytes_per_site(b, dt) * n
+        hbm_peak, peak_kind = peaks()
+        line = {
+            "metric": METRIC, "value": world * n * b / tt, "unit": "site*rhs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic (near-unit SU(3) links, Gaussian rhs)",
+            "config": {"workload": f"BASELINE configs[1] per GPU, weak-scaled over a T split: lattice {list(gdims)}",
+                       "lattice": list(gdims), "local": list(lg.dims), "nrhs": b, "m0": M0,
+                       "parallelism": f"T split x{world}, NCCL send/recv halos overlapped with interior slices",
+                       "l2": "2 rotating buffers of 403 MB (> L2)"},
+            "roofline": {"bound": "hbm", "achieved": alg / tt / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": alg / tt / 1e9 / hbm_peak, "traffic": None, "peak_kind": peak_kind},
+            "gpu_launches": 4 * args.steps, "clocks": clk,
+            "halo_bytes_per_step_per_rank": comm.stats["bytes_sent"] / max(1, comm.stats["applies"]),
+        }
+        print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -291,6 +358,14 @@ def main():
         return reference_arm(args)
     import torch
     import paper_2601_05816_b200 as P
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+        try:
+            multi_gpu(args, torch, P)
+        finally:
+            dist.destroy_process_group()
+        return
     torch.cuda.set_device(0)
     clocks = ClockSampler(0).start()
     sweep, hbm_peak, peak_kind = gpu_sweep(args, torch, P)

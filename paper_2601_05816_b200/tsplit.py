@@ -1,0 +1,218 @@
+"""Multi-GPU T split: the `comm=` seam of the reference (dirac.py:313-314, halo.py).
+
+One process per GPU (``torchrun --nproc-per-node N``), ``torch.distributed`` with
+the NCCL backend for the plumbing.  The lattice is split along T (direction 0,
+the slowest index), so each rank's slab is a contiguous range of sites and its
+links and fields are ordinary local device fields of extents (T/N, X, Y, Z).
+
+Per operator apply (halo.py:339-387 semantics, on the device):
+
+1. ``b200wd_halo_pack``: the lambda face (sign -1 half spinor of local slice 0)
+   and the chi face (U_0^H times the sign +1 half spinor of slice T_loc-1, link
+   applied at the source so no links travel), 6*b complex per face site;
+2. NCCL P2P: lambda -> rank-1, chi -> rank+1 (``batch_isend_irecv``), enqueued
+   right after the pack;
+3. the interior slices 1..T_loc-2 run concurrently with the transfers (they
+   never read a halo);
+4. after the receives complete, the two boundary slices consume the halos
+   (``b200wd_hop`` with ``lam_halo``/``chi_halo``).
+
+GMRES reductions are one ``all_reduce`` of the b partial sums per reducing pass.
+With one rank the split degenerates to the single-GPU periodic apply.
+The antiperiodic time boundary rides in the links of the rank that owns global
+slice T-1 (``fields.flip_time_boundary(..., t_global, t_origin)``).
+"""
+
+from __future__ import annotations
+
+import time
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .device import DeviceField, dtype_code, gauge_cache, ptr, require_device, stream_ptr, upload
+from .fields import SPINOR_LEN
+from .geometry import LatticeGeometry, t_split
+
+
+class CudaHaloKernels:
+    """Device kernels used by the T split (libb200wd)."""
+
+    def pack(self, lat, dtype, b, src_parity, gauge, src, lam, chi):
+        _lib.call("b200wd_halo_pack", lat, dtype_code(dtype), b, src_parity, gauge.ptr, src.ptr, ptr(lam), ptr(chi),
+                  stream_ptr())
+
+    def hop(self, lat, dtype, b, dst_parity, gauge, src, out, xself, alpha, beta, scale, t0, t1, lam=None, chi=None):
+        _lib.call("b200wd_hop", lat, dtype_code(dtype), b, dst_parity, gauge.ptr, src.ptr,
+                  None if xself is None else xself.ptr, out.ptr, float(alpha), float(beta), ptr(scale), int(t0),
+                  int(t1), ptr(lam), ptr(chi), stream_ptr())
+
+    def face_buffer(self, nf, b, dtype, device):
+        t = torch.complex128 if dtype == "c128" else torch.complex64
+        return torch.empty((6, nf, b), dtype=t, device=device)
+
+
+class TSplitComm:
+    """T-only domain decomposition over the ranks of a process group.
+
+    ``global_geom`` is the whole lattice; every rank owns slab
+    ``[rank*T/N, (rank+1)*T/N)`` (``local_geom``, ``t_origin``).  Fields given to
+    :meth:`apply_dirac` / :meth:`operator` are the rank-local slabs.
+    """
+
+    def __init__(self, global_geom: LatticeGeometry, group=None, kernels=None, device=None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.global_geom = global_geom
+        self.local_geom, self.t_origin = t_split(global_geom, self.world, self.rank)
+        if self.world > 1 and self.local_geom.dims[0] < 2:
+            raise ValueError("local T extent must be >= 2 (geometry.py:200-201)")
+        self.lat = _lib.Lattice.make(self.local_geom.dims, self.t_origin)
+        self.kernels = kernels or CudaHaloKernels()
+        self.device = device
+        self.up = (self.rank + 1) % self.world
+        self.down = (self.rank - 1) % self.world
+        self._faces = {}
+        self.stats = {"applies": 0, "bytes_sent": 0}
+
+    # -- plumbing -------------------------------------------------------------
+    def allreduce(self, t: torch.Tensor) -> torch.Tensor:
+        """Sum per-rank partial reductions (GMRES dots / norms) in place."""
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def _face_buffers(self, parity, b, dtype, device):
+        key = (parity, b, dtype)
+        if key not in self._faces:
+            nf = self.local_geom.sites_per_slice if parity is None else self.local_geom.sites_per_slice // 2
+            mk = lambda: self.kernels.face_buffer(nf, b, dtype, device)  # noqa: E731
+            self._faces[key] = {"lam": mk(), "chi": mk(), "lam_in": mk(), "chi_in": mk()}
+        return self._faces[key]
+
+    def exchange(self, lam: torch.Tensor, chi: torch.Tensor, lam_in: torch.Tensor, chi_in: torch.Tensor):
+        """lambda face -> rank-1, chi face -> rank+1; returns the work handles."""
+        if self.world == 1:
+            lam_in.copy_(lam)
+            chi_in.copy_(chi)
+            return []
+        ops = [
+            dist.P2POp(dist.isend, lam, self.down, self.group, tag=1),
+            dist.P2POp(dist.irecv, lam_in, self.up, self.group, tag=1),
+            dist.P2POp(dist.isend, chi, self.up, self.group, tag=2),
+            dist.P2POp(dist.irecv, chi_in, self.down, self.group, tag=2),
+        ]
+        self.stats["bytes_sent"] += 2 * lam.numel() * lam.element_size()
+        return dist.batch_isend_irecv(ops)
+
+    # -- the split hop ----------------------------------------------------------
+    def hop(self, dst_parity, src, out, xself, alpha, beta, scale=None, gauge=None):
+        """out = scale (alpha xself + beta H src) on the local slab with halos.
+
+        ``dst_parity`` None/-1 for full fields, else the parity of ``out``
+        (``src`` has the other parity)."""
+        gauge = gauge if gauge is not None else self.gauge
+        par = -1 if dst_parity is None else dst_parity
+        b, dtype = src.b, src.dtype
+        T = self.local_geom.dims[0]
+        k = self.kernels
+        if self.world == 1:
+            k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 0, T)
+            return out
+        f = self._face_buffers(None if par < 0 else 1 - par, b, dtype, src.data.device)
+        k.pack(self.lat, dtype, b, -1 if par < 0 else 1 - par, gauge, src, f["lam"], f["chi"])
+        reqs = self.exchange(f["lam"], f["chi"], f["lam_in"], f["chi_in"])
+        if T > 2:
+            k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 1, T - 1)
+        for r in reqs:
+            r.wait()
+        k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 0, 1, f["lam_in"], f["chi_in"])
+        k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, T - 1, T, f["lam_in"],
+              f["chi_in"])
+        self.stats["applies"] += 1
+        return out
+
+    # -- reference comm protocol ----------------------------------------------------
+    def bind(self, params, gauge, clover=None, dtype="c128"):
+        """Attach the local links (this rank's slab) and mass; returns self."""
+        from .dirac import _check_clover
+        _check_clover(clover)
+        if gauge.geom.dims != self.local_geom.dims:
+            raise ValueError(f"gauge slab {gauge.geom.dims} != local geometry {self.local_geom.dims}")
+        self.params = params
+        self.dtype = dtype
+        self.gauge = gauge_cache.get(gauge, dtype)
+        return self
+
+    def apply_device(self, v: DeviceField, out: DeviceField | None = None, scale=None) -> DeviceField:
+        out = v.empty_like() if out is None else out
+        return self.hop(None, v, out, v, 4.0 + self.params.m0, -1.0, scale)
+
+    def __call__(self, v):
+        if isinstance(v, DeviceField):
+            return self.apply_device(v)
+        return self.apply_device(upload(v, self.dtype)).to_host(v.layout)
+
+    def apply_dirac(self, params, gauge, clover, psi, flops=None, perf=None):
+        """dirac.py:313-314 seam: psi and gauge are this rank's T slab."""
+        if psi.s != SPINOR_LEN or psi.n_sites != self.local_geom.n_sites:
+            raise ValueError(f"field has {psi.n_sites} sites / s={psi.s}; local slab has "
+                             f"{self.local_geom.n_sites} sites")
+        t0 = time.perf_counter()
+        dtype = psi.dtype if isinstance(psi, DeviceField) else "c128"
+        self.bind(params, gauge, clover, dtype)
+        res = self(psi)
+        if flops is not None:
+            flops.add_apply(psi.n_sites, psi.b)
+        if perf is not None:
+            from .dirac import DiracPerfRecord, account_traffic
+            require_device()
+            torch.cuda.synchronize()
+            led = account_traffic(psi.b)
+            perf.append(DiracPerfRecord(time.perf_counter() - t0, psi.n_sites, psi.b, int(psi.layout),
+                                        led["flops_per_site"] * psi.n_sites, led["bytes_per_site"] * psi.n_sites))
+        return res
+
+    def operator(self, params, gauge, clover=None, dtype="c128"):
+        return self.bind(params, gauge, clover, dtype)
+
+    def schur(self, params, gauge, clover=None, dtype="c128", keep_parity=0):
+        """Distributed Schur operator (parity-restricted split hops)."""
+        from .oddeven import SchurOperator
+        self.bind(params, gauge, clover, dtype)
+        return SchurOperator(params, gauge, clover, keep_parity=keep_parity, dtype=dtype, lattice=self.lat,
+                             gauge_dev=self.gauge, comm=self)
+
+    def solve_dirac(self, params, gauge, clover, eta, cfg, odd_even=False, psi0=None):
+        """gmres.py:353-385 on the split lattice (eta: this rank's slab)."""
+        import numpy as np
+
+        from .blas import block_norm2_device
+        from .gmres import SolveReport, _sub, gmres_solve
+        from .oddeven import device_split
+        host = not isinstance(eta, DeviceField)
+        d_eta = upload(eta, "c128") if host else eta
+        op = self.operator(params, gauge, clover, "c128")
+        if not odd_even:
+            res = gmres_solve(op, d_eta, psi0, cfg)
+            psi, full = res.psi, res.final_relnorms
+        else:
+            schur = self.schur(params, gauge, clover, "c128")
+            keep, elim = device_split(self.lat, d_eta)
+            reduced = schur.reduce_rhs_device(keep, elim)
+            x0 = None
+            if psi0 is not None:
+                x0, _ = device_split(self.lat, upload(psi0) if not isinstance(psi0, DeviceField) else psi0)
+            res = gmres_solve(schur, reduced, x0, cfg)
+            x_elim = schur.reconstruct_device(res.psi, elim)
+            psi = schur.merge(res.psi, x_elim)
+            r = op.apply_device(psi)
+            rn = self.allreduce(block_norm2_device(_sub(d_eta, r)))
+            en = self.allreduce(block_norm2_device(d_eta))
+            en = np.sqrt(en.real.cpu().numpy())
+            full = np.where(en > 0, np.sqrt(rn.real.cpu().numpy()) / np.maximum(en, 1e-300), 0.0)
+        if host:
+            psi = psi.to_host(eta.layout)
+        return SolveReport(psi, res, odd_even, full, res.iterations)
