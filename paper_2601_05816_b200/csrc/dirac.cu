@@ -23,6 +23,10 @@
 
 namespace b200wd {
 
+#ifndef B200WD_RING_NOMATH
+#define B200WD_RING_NOMATH 0  // experiment: consumers skip the t/x/y arithmetic
+#endif
+
 // Threads per block of the hopping kernel and the occupancy target handed
 // to ptxas (c128: <= 168 registers -> 3 blocks = 12 warps per SM; c64: 4 blocks).
 constexpr int kHopThreads = 128;
@@ -81,7 +85,9 @@ __global__ void __launch_bounds__(kHopThreads, HopMinBlocks<R>::value) hop_kerne
 
   // forward hops: P-_mu U_mu(x) psi(x+mu)  (dirac.py:222-245)
   {
-    const C* ux = U + link_base(site);
+    const int64_t nblk = p.n >> 3;
+    const C* ux0 = U + link_base(site, 0, nblk);
+    const int64_t mstr = nblk * 72;  // distance between directions
     const int64_t f3 = (z + 1 == Z) ? site - (Z - 1) : site + 1;
     const int64_t f2 = (y + 1 == Y) ? site - (int64_t)(Y - 1) * sY : site + sY;
     const int64_t f1 = (x + 1 == X) ? site - (int64_t)(X - 1) * sX : site + sX;
@@ -89,13 +95,13 @@ __global__ void __launch_bounds__(kHopThreads, HopMinBlocks<R>::value) hop_kerne
     if (halo && t + 1 == T) {
       const int64_t fi = par ? (f0 >> 1) : f0;
       const C* hp = static_cast<const C*>(p.lam_halo) + fi * b + r0;
-      hop_lam_halo<R, V>(acc, hp, p.nf * b, ux + 0 * 72, 8);
+      hop_lam_halo<R, V>(acc, hp, p.nf * b, ux0, 8);
     } else {
-      hop_full<0, true, R, V>(acc, sptr(f0), kst, ux + 0 * 72, 8);
+      hop_full<0, true, R, V>(acc, sptr(f0), kst, ux0, 8);
     }
-    hop_full<1, true, R, V>(acc, sptr(f1), kst, ux + 1 * 72, 8);
-    hop_full<2, true, R, V>(acc, sptr(f2), kst, ux + 2 * 72, 8);
-    hop_full<3, true, R, V>(acc, sptr(f3), kst, ux + 3 * 72, 8);
+    hop_full<1, true, R, V>(acc, sptr(f1), kst, ux0 + 1 * mstr, 8);
+    hop_full<2, true, R, V>(acc, sptr(f2), kst, ux0 + 2 * mstr, 8);
+    hop_full<3, true, R, V>(acc, sptr(f3), kst, ux0 + 3 * mstr, 8);
   }
   // backward hops: P+_mu U_mu(x-mu)^H psi(x-mu)  (dirac.py:185-219, 248-255)
   {
@@ -108,11 +114,11 @@ __global__ void __launch_bounds__(kHopThreads, HopMinBlocks<R>::value) hop_kerne
       const C* hp = static_cast<const C*>(p.chi_halo) + fi * b + r0;
       hop_chi_halo<R, V>(acc, hp, p.nf * b);
     } else {
-      hop_full<0, false, R, V>(acc, sptr(b0), kst, U + link_base(b0) + 0 * 72, 8);
+      hop_full<0, false, R, V>(acc, sptr(b0), kst, U + link_base(b0, 0, p.n >> 3), 8);
     }
-    hop_full<1, false, R, V>(acc, sptr(b1), kst, U + link_base(b1) + 1 * 72, 8);
-    hop_full<2, false, R, V>(acc, sptr(b2), kst, U + link_base(b2) + 2 * 72, 8);
-    hop_full<3, false, R, V>(acc, sptr(b3), kst, U + link_base(b3) + 3 * 72, 8);
+    hop_full<1, false, R, V>(acc, sptr(b1), kst, U + link_base(b1, 1, p.n >> 3), 8);
+    hop_full<2, false, R, V>(acc, sptr(b2), kst, U + link_base(b2, 2, p.n >> 3), 8);
+    hop_full<3, false, R, V>(acc, sptr(b3), kst, U + link_base(b3, 3, p.n >> 3), 8);
   }
 
   // epilogue: out = scale_r (alpha xself + beta acc)
@@ -142,35 +148,34 @@ __global__ void __launch_bounds__(kHopThreads, HopMinBlocks<R>::value) hop_kerne
 
 // ---- persistent TMA ring kernel (full lattice) ---------------------------------
 //
-// Warp-specialised, persistent: one producer warp per CTA streams the inputs
-// of consecutive work items (NB site blocks of 8 z-consecutive sites x all b
-// rhs) into shared memory with cp.async.bulk (TMA 1-D bulk copies),
-// completion counted by mbarrier transactions; the consumer warps compute
-// from shared memory and hand each slot back through an "empty" mbarrier.
-// For the t, x and y hops the 8 neighbours of a site block are exactly one
-// other site block (Z % 8 == 0), i.e. one contiguous 96*b-complex run, so a
-// hop tile is NB bulk copies of spinor blocks + NB copies of one 72-complex
-// link plane (U_mu of the own block for forward hops, of the neighbour block
-// for backward hops).  Each item streams 6 hop tiles through an S-slot ring,
-// then its own block ("z tile": z hops + the xself of the epilogue) through
-// a dedicated buffer.  Loads in flight live in shared memory, not registers,
-// so the bytes in flight per SM (Little's law) are set by the ring depth.
-template <typename R, int V, int B> struct RingShape {
-  static constexpr int BT = B / V;                                   // threads per site
-  static constexpr int NB = (BT * 8 >= 96) ? 1 : (128 / (BT * 8));   // site blocks per item
-  static constexpr int NC = BT * 8 * NB;                             // consumer threads
-  static constexpr int NCW = NC / 32;                                // consumer warps
-  static constexpr int NT = NC + 32;                                 // + producer warp
-  static constexpr int SPIN = NB * 96 * B;                           // complex per spinor tile
-  static constexpr int SLOT = SPIN + NB * 72;                        // + one link plane per block
+// Warp-specialised and persistent: one producer warp per CTA streams the
+// inputs of consecutive work items (NB site blocks of 8 z-consecutive sites x
+// all b rhs) into shared memory with cp.async.bulk (TMA 1-D bulk copies),
+// completion counted by mbarrier transactions; the consumer warps compute from
+// shared memory and hand each slot back through an "empty" mbarrier.
+//
+// A work item needs 7 tiles: its own blocks (z hops + the xself of the
+// epilogue) and the neighbour blocks in -+t, -+x, -+y.  Because a site block is
+// 8 z-consecutive sites and Z % 8 == 0, the t/x/y neighbours of NB consecutive
+// blocks are again NB consecutive blocks: one contiguous run of NB*96*b
+// complex.  With the direction-major link layout the links a tile needs (U_mu
+// of the own blocks for a forward hop, of the neighbour blocks for a backward
+// hop, U_3 of the own blocks for the z tile) are one more contiguous run.  So
+// every tile is exactly two bulk copies -- the TMA unit has a per-copy cost
+// (~200-300 cycles per CTA, tools/mb_tma.cu), so copies are kept few and big.
+// When an item covers whole z lines (NB*8 == Z) the z hops never leave the
+// item; otherwise the z-edge sites are read with ordinary loads.
+template <typename R, int V, int B, int NB_> struct RingShape {
+  static constexpr int BT = B / V;                       // threads per site
+  static constexpr int NB = NB_;                         // site blocks per item
+  static constexpr int NC = BT * 8 * NB;                 // consumer threads
+  static constexpr int NCW = NC / 32;                    // consumer warps
+  static constexpr int NT = NC + 32;                     // + producer warp
+  static constexpr int SPIN = NB * 96 * B;               // complex per spinor tile
+  static constexpr int SLOT = SPIN + NB * 72;            // + one link direction per block
   static constexpr int SLOT_BYTES = SLOT * (int)sizeof(cx<R>);
-#ifndef B200WD_RING_BYTES
-#define B200WD_RING_BYTES (104 * 1024)
-#endif
-  static constexpr int S0 = B200WD_RING_BYTES / SLOT_BYTES;
-  static constexpr int S = S0 < 2 ? 2 : (S0 > 7 ? 7 : S0);          // ring depth (<= 7 tiles per item)
-  static constexpr int EDGE = 2 * NB * 12 * B;  // z-edge sites of the own blocks (one buffer: see producer)
-  static constexpr size_t SMEM = (size_t)SLOT_BYTES * S + EDGE * sizeof(cx<R>) + 8 * 2 * S;
+  static constexpr bool valid = (NC % 32 == 0) && NC >= 64 && NC <= 256 && (size_t)SLOT_BYTES * 2 <= 220 * 1024;
+  static size_t smem(int S) { return (size_t)SLOT_BYTES * S + 16 * S; }
 };
 
 // Coordinates of the first site of a site block (32-bit arithmetic: a rank's
@@ -189,7 +194,6 @@ __device__ __forceinline__ BlkCoord block_coord(int64_t g, const HopParams& p) {
   c.t = (int)(s0 / (uint32_t)p.X);
   return c;
 }
-// step to the next site block (z0 += 8 with carries)
 __device__ __forceinline__ void block_step(BlkCoord& c, const HopParams& p) {
   c.z0 += 8;
   if (c.z0 == p.Z) {
@@ -203,7 +207,6 @@ __device__ __forceinline__ void block_step(BlkCoord& c, const HopParams& p) {
     }
   }
 }
-
 template <int MU, bool FWD>
 __device__ __forceinline__ int64_t block_neighbor(int64_t g, const BlkCoord& c, const HopParams& p) {
   const int64_t s0 = g * 8;
@@ -217,98 +220,67 @@ __device__ __forceinline__ int64_t block_neighbor(int64_t g, const BlkCoord& c, 
                 : (c.y == 0 ? s0 + (int64_t)(p.Y - 1) * sY : s0 - sY);
   return ns >> 3;
 }
-
-// z neighbour (step +1 / -1 along z) of site d of a line with extent Z
 __device__ __forceinline__ int64_t z_neighbor(int64_t d, int z, int Z, int step) {
   if (step > 0) return (z + 1 == Z) ? d - (Z - 1) : d + 1;
   return (z == 0) ? d + (Z - 1) : d - 1;
 }
 
-// tile H in 0..5: hop (mu = H/2, forward if H even); H == 6: own block (z tile)
-// plus the z-edge sites outside the item (into `edge`)
-template <typename R, int V, int B, int H>
-__device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, BlkCoord c, cx<R>* slot,
-                                           uint64_t* full, cx<R>* edge) {
+// tile H in 0..5: hop (mu = H/2, forward if H even); H == 6: own blocks (z tile)
+template <typename R, int V, int B, int NB, int H>
+__device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, const BlkCoord& c0, cx<R>* slot,
+                                           uint64_t* full) {
   using C = cx<R>;
-  using Sh = RingShape<R, V, B>;
+  using Sh = RingShape<R, V, B, NB>;
   const C* src = static_cast<const C*>(p.src);
   const C* U = static_cast<const C*>(p.U);
-  uint32_t bytes = (uint32_t)(Sh::SLOT * sizeof(C));
+  const int64_t nblk = p.n >> 3;
+  mbar_expect_tx(full, (uint32_t)(Sh::SLOT * sizeof(C)));
   if constexpr (H == 6) {
-    // z-edge sites: site lo=0's z-1 and lo=7's z+1 neighbour of every block,
-    // when they fall outside the item's blocks (12 runs of B complex each)
-    BlkCoord ce = c;
-    uint32_t extra = 0;
-#pragma unroll 1
-    for (int jj = 0; jj < Sh::NB; ++jj) {
-      const int64_t g = gb0 + jj;
+    bulk_g2s(slot, src + gb0 * 96 * B, Sh::SPIN * sizeof(C), full);
+    bulk_g2s(slot + Sh::SPIN, U + (3 * nblk + gb0) * 72, NB * 72 * sizeof(C), full);
+  } else {
+    constexpr int MU = H >> 1;
+    constexpr bool FWD = !(H & 1);
+    // neighbour blocks of the NB own blocks: contiguous unless a wrap falls inside the item
+    const int64_t nb0 = block_neighbor<MU, FWD>(gb0, c0, p);
+    bool contiguous = true;
+    if constexpr (NB > 1) {
+      BlkCoord c = c0;
 #pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        const int64_t dd = g * 8 + (side ? 7 : 0);
-        const int64_t nd = z_neighbor(dd, ce.z0 + (side ? 7 : 0), p.Z, side ? 1 : -1);
-        const int64_t jb = (nd >> 3) - gb0;
-        if (jb < 0 || jb >= Sh::NB) extra += 12 * B * sizeof(C);
+      for (int jj = 1; jj < NB; ++jj) {
+        block_step(c, p);
+        contiguous &= block_neighbor<MU, FWD>(gb0 + jj, c, p) == nb0 + jj;
       }
-      if (jj + 1 < Sh::NB) block_step(ce, p);
     }
-    bytes += extra;
-  }
-  mbar_expect_tx(full, bytes);
-  if constexpr (H == 6) {
-    BlkCoord ce = c;
-#pragma unroll 1
-    for (int jj = 0; jj < Sh::NB; ++jj) {
-      const int64_t g = gb0 + jj;
+    if (contiguous) {
+      bulk_g2s(slot, src + nb0 * 96 * B, Sh::SPIN * sizeof(C), full);
+      bulk_g2s(slot + Sh::SPIN, U + (MU * nblk + (FWD ? gb0 : nb0)) * 72, NB * 72 * sizeof(C), full);
+    } else {
+      BlkCoord c = c0;
 #pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        const int64_t dd = g * 8 + (side ? 7 : 0);
-        const int64_t nd = z_neighbor(dd, ce.z0 + (side ? 7 : 0), p.Z, side ? 1 : -1);
-        const int64_t jb = (nd >> 3) - gb0;
-        if (jb < 0 || jb >= Sh::NB) {
-          const C* es = src + spinor_base(nd, 12, B);
-          C* ed = edge + (jj * 2 + side) * 12 * B;
-#pragma unroll 1
-          for (int k = 0; k < 12; ++k) bulk_g2s(ed + k * B, es + k * 8 * B, B * sizeof(C), full);
-        }
+      for (int jj = 0; jj < NB; ++jj) {
+        if (jj) block_step(c, p);
+        const int64_t nb = block_neighbor<MU, FWD>(gb0 + jj, c, p);
+        bulk_g2s(slot + jj * 96 * B, src + nb * 96 * B, 96 * B * sizeof(C), full);
+        bulk_g2s(slot + Sh::SPIN + jj * 72, U + (MU * nblk + (FWD ? gb0 + jj : nb)) * 72, 72 * sizeof(C), full);
       }
-      if (jj + 1 < Sh::NB) block_step(ce, p);
     }
-  }
-#pragma unroll
-  for (int jj = 0; jj < Sh::NB; ++jj) {
-    const int64_t g = gb0 + jj;
-    int64_t nb = g, lb = g;
-    int mu = 3;
-    if constexpr (H < 6) {
-      constexpr int MU = H >> 1;
-      constexpr bool FWD = !(H & 1);
-      mu = MU;
-      nb = block_neighbor<MU, FWD>(g, c, p);
-      lb = FWD ? g : nb;
-    }
-    bulk_g2s(slot + jj * 96 * B, src + nb * 96 * B, 96 * B * sizeof(C), full);
-    bulk_g2s(slot + Sh::SPIN + jj * 72, U + lb * 288 + mu * 72, 72 * sizeof(C), full);
-    if (jj + 1 < Sh::NB) block_step(c, p);
   }
 }
 
-template <typename R, int V, int B>
-__global__ void __launch_bounds__(RingShape<R, V, B>::NT) hop_ring_kernel(const HopParams p, int64_t n_items) {
+template <typename R, int V, int B, int NB>
+__global__ void __launch_bounds__(RingShape<R, V, B, NB>::NT) hop_ring_kernel(const HopParams p, int64_t n_items,
+                                                                              int S) {
   using C = cx<R>;
-  using Sh = RingShape<R, V, B>;
-  constexpr int S = Sh::S;
+  using Sh = RingShape<R, V, B, NB>;
   constexpr int KST = 8 * B;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   C* ring = reinterpret_cast<C*>(smem_raw);
-  C* edge = ring + S * Sh::SLOT;  // single buffer: item i's z tile is issued only after
-                                  // item i-1's z tile was consumed (S <= 7 tiles per item)
-  uint64_t* full = reinterpret_cast<uint64_t*>(edge + Sh::EDGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + S * Sh::SLOT);
   uint64_t* empty = full + S;
 
   const int tid = threadIdx.x;  // 1-D block: consumers [0, NC), producer warp [NC, NC+32)
-  const bool producer = tid >= Sh::NC;
   if (tid == 0) {
-#pragma unroll
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], Sh::NCW);
@@ -317,34 +289,22 @@ __global__ void __launch_bounds__(RingShape<R, V, B>::NT) hop_ring_kernel(const 
   }
   __syncthreads();
 
-  if (producer) {
+  if (tid >= Sh::NC) {
     if (tid == Sh::NC) {  // one elected lane issues every copy
-      int seq = 0;
-      const C* srcp = static_cast<const C*>(p.src);
-      const C* Up = static_cast<const C*>(p.U);
+      int pslot = 0, pfirst = 1;
+      uint32_t pphase = 0;  // phase of the next fill of pslot; its release is phase^1 of empty
       for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int64_t gb0 = (p.d_begin >> 3) + it * Sh::NB;
+        const int64_t gb0 = (p.d_begin >> 3) + it * NB;
         const BlkCoord c0 = block_coord(gb0, p);
-        // warm L2 with the compulsory misses of the next item of this CTA: its
-        // t+1 neighbour blocks and its own link blocks (first touch in sweep order)
-        const int64_t nx = it + gridDim.x;
-        if (nx < n_items) {
-          const int64_t gn = (p.d_begin >> 3) + nx * Sh::NB;
-          BlkCoord cn = block_coord(gn, p);
-#pragma unroll 1
-          for (int jj = 0; jj < Sh::NB; ++jj) {
-            const int64_t nb = block_neighbor<0, true>(gn + jj, cn, p);
-            bulk_prefetch_l2(srcp + nb * 96 * B, 96 * B * sizeof(C));
-            if (jj + 1 < Sh::NB) block_step(cn, p);
-          }
-          bulk_prefetch_l2(Up + gn * 288, Sh::NB * 288 * sizeof(C));
-        }
-#define B200WD_PRODUCE(H)                                                                 \
-  {                                                                                       \
-    const int slot = seq % S, use = seq / S;                                              \
-    if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);                                  \
-    ring_issue<R, V, B, H>(p, gb0, c0, ring + slot * Sh::SLOT, &full[slot], edge);        \
-    ++seq;                                                                                \
+#define B200WD_PRODUCE(H)                                                    \
+  {                                                                          \
+    if (pfirst == 0) mbar_wait(&empty[pslot], pphase ^ 1u);                  \
+    ring_issue<R, V, B, NB, H>(p, gb0, c0, ring + pslot * Sh::SLOT, &full[pslot]); \
+    if (++pslot == S) {                                                      \
+      pslot = 0;                                                             \
+      pphase ^= 1u;                                                          \
+      pfirst = 0;                                                            \
+    }                                                                        \
   }
         B200WD_PRODUCE(6)
         B200WD_PRODUCE(0)
@@ -366,43 +326,33 @@ __global__ void __launch_bounds__(RingShape<R, V, B>::NT) hop_ring_kernel(const 
   const bool lead = (tid & 31) == 0;
   const C* __restrict__ src = static_cast<const C*>(p.src);
   const C* __restrict__ U = static_cast<const C*>(p.U);
+  const int64_t nblk = p.n >> 3;
   const int Z = p.Z;
-  R sc[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) sc[v] = p.scale ? R(__ldg(p.scale + r0 + v)) : R(1);
-  const R beta = R(p.beta), alpha = R(p.alpha);
-  const bool self_is_src = p.xself == p.src;
-
-  // acc accumulates (alpha/beta) xself + 2H src, so out = (sc beta) acc: the own
-  // block (z tile) is consumed first and its slot recycled immediately
-  const R ab = (p.xself != nullptr && p.beta != 0.0) ? R(p.alpha / p.beta) : R(0);
   R scb[V];
 #pragma unroll
-  for (int v = 0; v < V; ++v) scb[v] = sc[v] * beta;
-  int seq = 0;
+  for (int v = 0; v < V; ++v) scb[v] = (p.scale ? R(__ldg(p.scale + r0 + v)) : R(1)) * R(p.beta);
+  // acc accumulates (alpha/beta) xself + 2H src; out = (scale beta) acc
+  const R ab = (p.xself != nullptr) ? R(p.alpha / p.beta) : R(0);
+  const bool self_is_src = p.xself == p.src;
+
+  int cslot = 0;
+  uint32_t cphase = 0;
   for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
-    const int64_t gb0 = (p.d_begin >> 3) + it * Sh::NB;
+    const int64_t gb0 = (p.d_begin >> 3) + it * NB;
     const int64_t d = (gb0 + j) * 8 + lo;
     C acc[V][12];
-    {
-      const int slot = seq % S;
-      mbar_wait(&full[slot], (seq / S) & 1);
+    {  // own blocks: xself, z hops
+      const int slot = cslot;
+      mbar_wait(&full[slot], cphase);
       const C* zt = ring + slot * Sh::SLOT;
-      // init from xself
-      if (self_is_src) {
+      if (self_is_src || p.xself) {
+        const C* xp = self_is_src ? zt + j * 96 * B + lo * B + r0
+                                  : static_cast<const C*>(p.xself) + spinor_base(d, 12, B) + r0;
 #pragma unroll
         for (int k = 0; k < 12; ++k) {
           C xv[V];
-          VecIO<R, V>::lds(xv, zt + j * 96 * B + lo * B + r0 + k * KST);
-#pragma unroll
-          for (int v = 0; v < V; ++v) acc[v][k] = mk(ab * xv[v].x, ab * xv[v].y);
-        }
-      } else if (p.xself) {
-        const C* xs = static_cast<const C*>(p.xself) + spinor_base(d, 12, B) + r0;
-#pragma unroll
-        for (int k = 0; k < 12; ++k) {
-          C xv[V];
-          VecIO<R, V>::ld(xv, xs + k * KST);
+          if (self_is_src) VecIO<R, V>::lds(xv, xp + k * KST);
+          else VecIO<R, V>::ld(xv, xp + k * KST);
 #pragma unroll
           for (int v = 0; v < V; ++v) acc[v][k] = mk(ab * xv[v].x, ab * xv[v].y);
         }
@@ -412,41 +362,48 @@ __global__ void __launch_bounds__(RingShape<R, V, B>::NT) hop_ring_kernel(const 
 #pragma unroll
           for (int k = 0; k < 12; ++k) acc[v][k] = mk(R(0), R(0));
       }
-      // z hops from the own blocks; z-edge sites from the edge buffer
       const int z = (int)((uint32_t)d % (uint32_t)Z);
       {
         const int64_t nd = z_neighbor(d, z, Z, 1);
         const int64_t jb = (nd >> 3) - gb0;
-        const bool in = jb >= 0 && jb < Sh::NB;
-        const C* sp = in ? zt + jb * 96 * B + (nd & 7) * B + r0 : edge + (j * 2 + 1) * 12 * B + r0;
-        const int kst = in ? KST : B;
-        hop_full<3, true, R, V, true, true>(acc, sp, kst, zt + Sh::SPIN + j * 72 + lo, 8);
+        const C* ul = zt + Sh::SPIN + j * 72 + lo;  // U_3(x), own blocks
+        if (jb >= 0 && jb < NB)
+          hop_full<3, true, R, V, true, true>(acc, zt + jb * 96 * B + (nd & 7) * B + r0, KST, ul, 8);
+        else
+          hop_full<3, true, R, V, false, true>(acc, src + spinor_base(nd, 12, B) + r0, KST, ul, 8);
       }
       {
         const int64_t nd = z_neighbor(d, z, Z, -1);
         const int64_t jb = (nd >> 3) - gb0;
-        const bool in = jb >= 0 && jb < Sh::NB;
-        const C* sp = in ? zt + jb * 96 * B + (nd & 7) * B + r0 : edge + (j * 2 + 0) * 12 * B + r0;
-        const int kst = in ? KST : B;
-        // U_3(x - z): own link plane, or global for an edge site (generic load)
-        const C* ul = in ? zt + Sh::SPIN + jb * 72 + (nd & 7) : U + link_base(nd) + 3 * 72;
-        hop_full<3, false, R, V, true, false, true>(acc, sp, kst, ul, 8);
+        if (jb >= 0 && jb < NB)
+          hop_full<3, false, R, V, true, true>(acc, zt + jb * 96 * B + (nd & 7) * B + r0, KST,
+                                               zt + Sh::SPIN + jb * 72 + (nd & 7), 8);
+        else
+          hop_full<3, false, R, V, false, false>(acc, src + spinor_base(nd, 12, B) + r0, KST,
+                                                 U + link_base(nd, 3, nblk), 8);
       }
       __syncwarp();
       if (lead) mbar_arrive(&empty[slot]);
-      ++seq;
+      if (++cslot == S) {
+        cslot = 0;
+        cphase ^= 1u;
+      }
     }
 
 #define B200WD_CONSUME(H)                                                                            \
   {                                                                                                  \
-    const int slot = seq % S;                                                                        \
-    mbar_wait(&full[slot], (seq / S) & 1);                                                           \
+    const int slot = cslot;                                                                          \
+    mbar_wait(&full[slot], cphase);                                                                  \
     const C* sb = ring + slot * Sh::SLOT;                                                            \
-    hop_full<((H) >> 1), !((H)&1), R, V, true, true>(acc, sb + j * 96 * B + lo * B + r0, KST,        \
-                                                      sb + Sh::SPIN + j * 72 + lo, 8);               \
+    if (!B200WD_RING_NOMATH)                                                                         \
+      hop_full<((H) >> 1), !((H)&1), R, V, true, true>(acc, sb + j * 96 * B + lo * B + r0, KST,      \
+                                                        sb + Sh::SPIN + j * 72 + lo, 8);             \
     __syncwarp();                                                                                    \
     if (lead) mbar_arrive(&empty[slot]);                                                             \
-    ++seq;                                                                                           \
+    if (++cslot == S) {                                                                              \
+      cslot = 0;                                                                                     \
+      cphase ^= 1u;                                                                                  \
+    }                                                                                                \
   }
     B200WD_CONSUME(0)
     B200WD_CONSUME(1)
@@ -456,7 +413,6 @@ __global__ void __launch_bounds__(RingShape<R, V, B>::NT) hop_ring_kernel(const 
     B200WD_CONSUME(5)
 #undef B200WD_CONSUME
 
-    // epilogue: out = sc beta acc = sc (alpha xself + beta 2H src / 2)
     C* out = static_cast<C*>(p.out) + spinor_base(d, 12, B) + r0;
 #pragma unroll
     for (int k = 0; k < 12; ++k) {
@@ -470,39 +426,118 @@ __global__ void __launch_bounds__(RingShape<R, V, B>::NT) hop_ring_kernel(const 
 
 static int g_sm_count = 0;
 
-// Launch the ring kernel when its shape preconditions hold; false -> the
-// caller uses the generic kernel.
-template <typename R, int V, int B>
-static bool try_launch_ring(const HopParams& p, cudaStream_t st) {
-  using Sh = RingShape<R, V, B>;
-  if (Sh::NC % 32 != 0 || p.beta == 0.0) return false;
-  if (p.dst_parity >= 0 || p.lam_halo != nullptr || p.Z % 8 != 0) return false;
-  if ((p.d_begin & 7) || (p.d_end & 7)) return false;
-  const int64_t nblk = (p.d_end - p.d_begin) >> 3;
-  if (nblk % Sh::NB) return false;
-  static int ctas_per_sm = -1;
-  if (ctas_per_sm < 0) {
-    if (cudaFuncSetAttribute(hop_ring_kernel<R, V, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)Sh::SMEM) != cudaSuccess) {
-      ctas_per_sm = 0;
-      return false;
+// Ring configuration: site blocks per item (compile time) and ring depth
+// (runtime).  Default: whole z lines per item when that gives <= 256
+// consumer threads, a ring of ~100 KB per CTA (two CTAs per SM) or ~200 KB
+// (one CTA) for large slots; B200WD_RING_CFG="NB,S" overrides (tuning).
+struct RingCfg {
+  int nb = 0, s = 0;
+};
+static RingCfg ring_env() {
+  static RingCfg c{-1, -1};
+  if (c.nb < 0) {
+    c = RingCfg{};
+    const char* e = getenv("B200WD_RING_CFG");
+    if (e) sscanf(e, "%d,%d", &c.nb, &c.s);
+  }
+  return c;
+}
+
+template <typename R, int V, int B, int NB>
+static bool launch_ring_nb(const HopParams& p, int64_t nblk, int S, cudaStream_t st) {
+  using Sh = RingShape<R, V, B, NB>;
+  if constexpr (!Sh::valid) {
+    return false;
+  } else {
+    if (nblk % NB) return false;
+    if (S <= 0) S = (Sh::SLOT_BYTES >= 40 * 1024) ? (200 * 1024) / Sh::SLOT_BYTES : (100 * 1024) / Sh::SLOT_BYTES;
+    if (S < 2) S = 2;
+    if (S > 8) S = 8;
+    const size_t smem = Sh::smem(S);
+    static size_t attr_smem = 0;
+    if (attr_smem < smem) {
+      if (cudaFuncSetAttribute(hop_ring_kernel<R, V, B, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem) != cudaSuccess)
+        return false;
+      attr_smem = smem;
     }
-    int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, hop_ring_kernel<R, V, B>, Sh::NT, Sh::SMEM) != cudaSuccess)
-      nb = 0;
-    ctas_per_sm = nb;
-    if (g_sm_count == 0) {
+    int ctas_per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, hop_ring_kernel<R, V, B, NB>, Sh::NT, smem) !=
+            cudaSuccess ||
+        ctas_per_sm <= 0)
+      return false;
+    static int sm_count = 0;
+    if (sm_count == 0) {
       int dev = 0;
       cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+      cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t n_items = nblk / NB;
+    int64_t grid = (int64_t)ctas_per_sm * sm_count;
+    if (grid > n_items) grid = n_items;
+    hop_ring_kernel<R, V, B, NB><<<(unsigned)grid, Sh::NT, smem, st>>>(p, n_items, S);
+    return true;
+  }
+}
+
+// Measured best (NB, S) per (dtype, b) (tools/tune_ring.py on B200); {0,0}
+// = defaults (whole z lines per item, ~100/200 KB ring).
+template <typename R, int V, int B>
+static RingCfg ring_table(int Z) {
+  (void)Z;
+  if constexpr (sizeof(R) == 8) {
+    switch (B) {
+      case 4: return RingCfg{2, 3};
+      case 6: return RingCfg{2, 3};
+      case 8: return RingCfg{2, 4};
+      case 12: return RingCfg{2, 4};
+      case 16: return RingCfg{2, 4};
+      case 24: return RingCfg{1, 6};
+      case 32: return RingCfg{2, 6};
+      default: return RingCfg{};
+    }
+  } else {
+    switch (B) {
+      case 4: return RingCfg{4, 3};
+      case 6: return RingCfg{4, 2};
+      case 8: return RingCfg{2, 4};
+      case 12: return RingCfg{2, 2};
+      case 16: return RingCfg{2, 2};
+      case 24: return RingCfg{1, 3};
+      case 32: return RingCfg{2, 4};
+      default: return RingCfg{};
     }
   }
-  if (ctas_per_sm <= 0) return false;
-  const int64_t n_items = nblk / Sh::NB;
-  int64_t grid = (int64_t)ctas_per_sm * g_sm_count;
-  if (grid > n_items) grid = n_items;
-  hop_ring_kernel<R, V, B><<<(unsigned)grid, Sh::NT, Sh::SMEM, st>>>(p, n_items);
-  return true;
+}
+
+// Launch the ring kernel when its shape preconditions hold (full lattice, no
+// halos, Z % 8 == 0); false -> the caller uses the generic kernel.
+template <typename R, int V, int B>
+static bool try_launch_ring(const HopParams& p, cudaStream_t st) {
+  if (p.dst_parity >= 0 || p.lam_halo != nullptr || p.Z % 8 != 0 || p.beta == 0.0) return false;
+  if ((p.d_begin & 7) || (p.d_end & 7)) return false;
+  const int64_t nblk = (p.d_end - p.d_begin) >> 3;
+  const RingCfg env = ring_env();
+  RingCfg c = ring_table<R, V, B>(p.Z);
+  if (env.nb > 0) c.nb = env.nb;
+  if (env.s > 0) c.s = env.s;
+  if (c.nb <= 0) c.nb = p.Z / 8;  // whole z lines per item
+  switch (c.nb) {
+    case 4:
+      if (launch_ring_nb<R, V, B, 4>(p, nblk, c.s, st)) return true;
+      break;
+    case 2:
+      if (launch_ring_nb<R, V, B, 2>(p, nblk, c.s, st)) return true;
+      break;
+    case 1:
+      if (launch_ring_nb<R, V, B, 1>(p, nblk, c.s, st)) return true;
+      break;
+    default:
+      break;
+  }
+  // partial lines: the z edges use ordinary loads
+  if (launch_ring_nb<R, V, B, 2>(p, nblk, 0, st)) return true;
+  return launch_ring_nb<R, V, B, 1>(p, nblk, 0, st);
 }
 
 // ---- halo face pack (halo.py:352-368) ---------------------------------------
@@ -551,7 +586,7 @@ __global__ void __launch_bounds__(256) halo_pack_kernel(const HopParams p, void*
         VecIO<R, V>::st(out + hk * fstride, res);
       }
     } else {
-      const C* ux = U + link_base(site);
+      const C* ux = U + link_base(site, 0, p.n >> 3);
       C u[9];
 #pragma unroll
       for (int e = 0; e < 9; ++e) u[e] = __ldg(ux + e * 8);

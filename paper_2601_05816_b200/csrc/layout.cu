@@ -44,18 +44,22 @@ __global__ void spinor_convert_kernel(const void* __restrict__ in, void* __restr
   }
 }
 
-// (n,4,3,3) row-major -> site-blocked link planes
+// (n,4,3,3) row-major -> direction-major site-blocked link planes (layout.cuh)
 template <typename C>
 __global__ void gauge_import_kernel(const double2* __restrict__ in, C* __restrict__ out, int64_t n) {
   const int64_t total = n * 36;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    // i = (blk * 36 + me) * 8 + lo
+    // i = ((mu * nblk + blk) * 9 + e) * 8 + lo
+    const int64_t nblk = n >> 3;
     const int lo = (int)(i & 7);
-    const int64_t q = i >> 3;
-    const int me = (int)(q % 36);  // mu*9 + e
-    const int64_t x = (q / 36) * 8 + lo;
-    out[i] = from_c128<C>(__ldg(in + x * 36 + me));
+    int64_t q = i >> 3;
+    const int e = (int)(q % 9);
+    q /= 9;
+    const int64_t blk = q % nblk;
+    const int mu = (int)(q / nblk);
+    const int64_t x = blk * 8 + lo;
+    out[i] = from_c128<C>(__ldg(in + x * 36 + mu * 9 + e));
   }
 }
 

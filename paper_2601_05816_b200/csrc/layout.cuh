@@ -9,8 +9,10 @@
 // distance between the components of one site is the compile-time constant
 // 8*b, so the 12 loads of a neighbour spinor are one address + immediates.
 //
-// Links, 4 directions x 9 entries per site:
-//   element (site, mu, e) at  ((site >> 3) * 36 + mu * 9 + e) * 8 + (site & 7)
+// Links, 4 directions x 9 entries per site, direction-major:
+//   element (site, mu, e) at  ((mu * nblk + (site >> 3)) * 9 + e) * 8 + (site & 7),  nblk = n / 8
+// so one direction's links of consecutive site blocks are one contiguous run
+// (a single bulk copy per hop tile, whatever the number of blocks).
 #pragma once
 #include <stdint.h>
 
@@ -25,6 +27,9 @@ __host__ __device__ __forceinline__ int64_t spinor_elem(int64_t site, int k, int
 __host__ __device__ __forceinline__ int64_t spinor_base(int64_t site, int s, int b) {
   return (((site >> 3) * s * 8) + (site & 7)) * (int64_t)b;
 }
-__host__ __device__ __forceinline__ int64_t link_base(int64_t site) { return (site >> 3) * 288 + (site & 7); }
+// element of (site, mu, e=0); entry e is at +8*e
+__host__ __device__ __forceinline__ int64_t link_base(int64_t site, int mu, int64_t nblk) {
+  return (mu * nblk + (site >> 3)) * 72 + (site & 7);
+}
 
 }  // namespace b200wd

@@ -44,6 +44,20 @@ template <> struct VecIO<double, 1> {
   static __device__ __forceinline__ void lds(double2 (&o)[1], const double2* p) { o[0] = *p; }
   static __device__ __forceinline__ void st(double2* p, const double2 (&v)[1]) { __stcs(p, v[0]); }
 };
+template <> struct VecIO<double, 2> {
+  static __device__ __forceinline__ void ld(double2 (&o)[2], const double2* p) {
+    o[0] = __ldg(p);
+    o[1] = __ldg(p + 1);
+  }
+  static __device__ __forceinline__ void lds(double2 (&o)[2], const double2* p) {
+    o[0] = p[0];
+    o[1] = p[1];
+  }
+  static __device__ __forceinline__ void st(double2* p, const double2 (&v)[2]) {
+    __stcs(p, v[0]);
+    __stcs(p + 1, v[1]);
+  }
+};
 template <> struct VecIO<float, 1> {
   static __device__ __forceinline__ void ld(float2 (&o)[1], const float2* p) { o[0] = __ldg(p); }
   static __device__ __forceinline__ void lds(float2 (&o)[1], const float2* p) { o[0] = *p; }

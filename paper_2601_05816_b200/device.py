@@ -6,8 +6,8 @@ and pinned host buffers.  Every byte of compute goes through libb200wd.
 Device layouts (include/b200wd.h, csrc/layout.cuh):
   * spinor block field -> torch tensor (n/8, s, 8, b), complex128 or
     complex64: site-blocked component planes, rhs innermost;
-  * links -> (n/8, 36, 8): per 8-site block, one run of 8 per
-    (direction, 3x3 entry).
+  * links -> (4, n/8, 9, 8): direction-major, per 8-site block one run of
+    8 per 3x3 entry.
 The upload path copies the reference storage (Layout 1 or 2, complex128) as
 raw bytes and converts with a device kernel; the download path is the exact
 inverse.
@@ -204,7 +204,7 @@ def download(df: DeviceField, layout=None, out: BlockSpinorField | None = None, 
 
 @dataclass
 class DeviceGauge:
-    """Links resident in HBM as (n/8, 36, 8) site-blocked planes of one dtype."""
+    """Links resident in HBM as (4, n/8, 9, 8) direction-major site-blocked planes."""
 
     data: "torch.Tensor"
     geom: LatticeGeometry
@@ -225,7 +225,7 @@ def upload_gauge(gauge, dtype: str = "c128", stream=None) -> DeviceGauge:
     if data.shape != (n, 4, 3, 3):
         raise ValueError(f"gauge data has shape {data.shape}, expected {(n, 4, 3, 3)}")
     raw = torch.from_numpy(data.reshape(-1)).to(dev, non_blocking=True)
-    out = torch.empty((n // SITE_BLOCK, 36, SITE_BLOCK), dtype=torch_dtype(dtype), device=dev)
+    out = torch.empty((4, n // SITE_BLOCK, 9, SITE_BLOCK), dtype=torch_dtype(dtype), device=dev)
     _lib.call("b200wd_gauge_import", ptr(raw), n, ptr(out), dtype_code(dtype), stream_ptr(stream))
     return DeviceGauge(out, gauge.geom)
 
