@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libb200wd.so"
-SOURCES = ["capi.cu", "layout.cu", "dirac.cu", "blas.cu"]
+SOURCES = ["capi.cu", "layout.cu", "dirac.cu", "dirac_c128.cu", "dirac_c64.cu", "blas.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -46,15 +46,18 @@ def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: 
     tmp = PKG / "build" / ("_".join(defines) or "default")
     tmp.mkdir(parents=True, exist_ok=True)
     logs = []
-    for src in SOURCES:
+    procs = []
+    for src in SOURCES:  # translation units compile in parallel
         obj = tmp / (Path(src).stem + ".o")
         cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(ROOT / "include"), "-I", str(CSRC),
                "-c", str(CSRC / src), "-o", str(obj)]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(r.stderr)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
+        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
         objs.append(str(obj))
+    for src, pr in procs:
+        _, err = pr.communicate()
+        logs.append(err)
+        if pr.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src}:\n{err}")
     cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC",
            *objs, "-o", str(lib) + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -14,664 +14,9 @@
 // and finally writes  out = scale_r (alpha * xself + beta * H src)  once.
 // Neither lambda nor chi (the reference's 8 materialised half-spinor fields,
 // dirac.py:273-296) ever touches memory.
-#include <cstdlib>
-
-#include "capi.cuh"
-#include "common.cuh"
-#include "layout.cuh"
-#include "stencil.cuh"
+#include "dirac_kernels.cuh"
 
 namespace b200wd {
-
-#ifndef B200WD_RING_NOMATH
-#define B200WD_RING_NOMATH 0  // experiment: consumers skip the t/x/y arithmetic
-#endif
-
-// Threads per block of the hopping kernel and the occupancy target handed
-// to ptxas (c128: <= 168 registers -> 3 blocks = 12 warps per SM; c64: 4 blocks).
-constexpr int kHopThreads = 128;
-#ifndef B200WD_MINB_C128
-#define B200WD_MINB_C128 3
-#endif
-#ifndef B200WD_MINB_C64
-#define B200WD_MINB_C64 4
-#endif
-template <typename R> struct HopMinBlocks;
-template <> struct HopMinBlocks<double> { static constexpr int value = B200WD_MINB_C128; };
-template <> struct HopMinBlocks<float> { static constexpr int value = B200WD_MINB_C64; };
-
-// B > 0: rhs count known at compile time (all component / link strides are
-// immediates); B == 0: runtime rhs count.
-template <typename R, int V, int B>
-__global__ void __launch_bounds__(kHopThreads, HopMinBlocks<R>::value) hop_kernel(const HopParams p) {
-  using C = cx<R>;
-  const int64_t d = p.d_begin + (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
-  if (d >= p.d_end) return;
-  const int b = B > 0 ? B : p.b;
-  const int r0 = threadIdx.x * V;
-  const int Z = p.Z, Y = p.Y, X = p.X, T = p.T;
-  const bool par = p.dst_parity >= 0;
-
-  // natural site and its coordinates (geometry.py:51-72)
-  int64_t site = par ? 2 * d : d;
-  int z = (int)(site % Z);
-  int64_t q = site / Z;
-  const int y = (int)(q % Y);
-  q /= Y;
-  const int x = (int)(q % X);
-  const int t = (int)(q / X);
-  if (par) {
-    const int zz = z + ((t + x + y + z + p.par0 + p.dst_parity) & 1);
-    site += zz - z;
-    z = zz;
-  }
-  const int64_t sY = Z, sX = (int64_t)Y * Z, sT = p.per_t;
-
-  const C* __restrict__ src = static_cast<const C*>(p.src);
-  const C* __restrict__ U = static_cast<const C*>(p.U);
-  const int kst = 8 * b;  // component stride (elements)
-
-  C acc[V][12];
-#pragma unroll
-  for (int v = 0; v < V; ++v)
-#pragma unroll
-    for (int k = 0; k < 12; ++k) acc[v][k] = mk(R(0), R(0));
-
-  auto sptr = [&](int64_t s) {
-    const int64_t i = par ? (s >> 1) : s;
-    return src + spinor_base(i, 12, b) + r0;
-  };
-  const bool halo = p.lam_halo != nullptr;
-
-  // forward hops: P-_mu U_mu(x) psi(x+mu)  (dirac.py:222-245)
-  {
-    const int64_t nblk = p.n >> 3;
-    const C* ux0 = U + link_base(site, 0, nblk);
-    const int64_t mstr = nblk * 72;  // distance between directions
-    const int64_t f3 = (z + 1 == Z) ? site - (Z - 1) : site + 1;
-    const int64_t f2 = (y + 1 == Y) ? site - (int64_t)(Y - 1) * sY : site + sY;
-    const int64_t f1 = (x + 1 == X) ? site - (int64_t)(X - 1) * sX : site + sX;
-    const int64_t f0 = (t + 1 == T) ? site - (int64_t)(T - 1) * sT : site + sT;
-    if (halo && t + 1 == T) {
-      const int64_t fi = par ? (f0 >> 1) : f0;
-      const C* hp = static_cast<const C*>(p.lam_halo) + fi * b + r0;
-      hop_lam_halo<R, V>(acc, hp, p.nf * b, ux0, 8);
-    } else {
-      hop_full<0, true, R, V>(acc, sptr(f0), kst, ux0, 8);
-    }
-    hop_full<1, true, R, V>(acc, sptr(f1), kst, ux0 + 1 * mstr, 8);
-    hop_full<2, true, R, V>(acc, sptr(f2), kst, ux0 + 2 * mstr, 8);
-    hop_full<3, true, R, V>(acc, sptr(f3), kst, ux0 + 3 * mstr, 8);
-  }
-  // backward hops: P+_mu U_mu(x-mu)^H psi(x-mu)  (dirac.py:185-219, 248-255)
-  {
-    const int64_t b3 = (z == 0) ? site + (Z - 1) : site - 1;
-    const int64_t b2 = (y == 0) ? site + (int64_t)(Y - 1) * sY : site - sY;
-    const int64_t b1 = (x == 0) ? site + (int64_t)(X - 1) * sX : site - sX;
-    const int64_t b0 = (t == 0) ? site + (int64_t)(T - 1) * sT : site - sT;
-    if (halo && t == 0) {
-      const int64_t fi = par ? (site >> 1) : site;
-      const C* hp = static_cast<const C*>(p.chi_halo) + fi * b + r0;
-      hop_chi_halo<R, V>(acc, hp, p.nf * b);
-    } else {
-      hop_full<0, false, R, V>(acc, sptr(b0), kst, U + link_base(b0, 0, p.n >> 3), 8);
-    }
-    hop_full<1, false, R, V>(acc, sptr(b1), kst, U + link_base(b1, 1, p.n >> 3), 8);
-    hop_full<2, false, R, V>(acc, sptr(b2), kst, U + link_base(b2, 2, p.n >> 3), 8);
-    hop_full<3, false, R, V>(acc, sptr(b3), kst, U + link_base(b3, 3, p.n >> 3), 8);
-  }
-
-  // epilogue: out = scale_r (alpha xself + beta acc)
-  const int64_t o = spinor_base(d, 12, b) + r0;
-  C* out = static_cast<C*>(p.out) + o;
-  const C* xs = p.xself ? static_cast<const C*>(p.xself) + o : nullptr;
-  R sc[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) sc[v] = p.scale ? R(__ldg(p.scale + r0 + v)) : R(1);
-  const R beta = R(p.beta), alpha = R(p.alpha);
-#pragma unroll
-  for (int k = 0; k < 12; ++k) {
-    C res[V];
-    if (xs) {
-      C xv[V];
-      VecIO<R, V>::ld(xv, xs + k * kst);
-#pragma unroll
-      for (int v = 0; v < V; ++v)
-        res[v] = mk(sc[v] * (alpha * xv[v].x + beta * acc[v][k].x), sc[v] * (alpha * xv[v].y + beta * acc[v][k].y));
-    } else {
-#pragma unroll
-      for (int v = 0; v < V; ++v) res[v] = mk(sc[v] * beta * acc[v][k].x, sc[v] * beta * acc[v][k].y);
-    }
-    VecIO<R, V>::st(out + k * kst, res);
-  }
-}
-
-// ---- persistent TMA ring kernel (full lattice) ---------------------------------
-//
-// Warp-specialised and persistent: one producer warp per CTA streams the
-// inputs of consecutive work items (NB site blocks of 8 z-consecutive sites x
-// all b rhs) into shared memory with cp.async.bulk (TMA 1-D bulk copies),
-// completion counted by mbarrier transactions; the consumer warps compute from
-// shared memory and hand each slot back through an "empty" mbarrier.
-//
-// A work item needs 7 tiles: its own blocks (z hops + the xself of the
-// epilogue) and the neighbour blocks in -+t, -+x, -+y.  Because a site block is
-// 8 z-consecutive sites and Z % 8 == 0, the t/x/y neighbours of NB consecutive
-// blocks are again NB consecutive blocks: one contiguous run of NB*96*b
-// complex.  With the direction-major link layout the links a tile needs (U_mu
-// of the own blocks for a forward hop, of the neighbour blocks for a backward
-// hop, U_3 of the own blocks for the z tile) are one more contiguous run.  So
-// every tile is exactly two bulk copies -- the TMA unit has a per-copy cost
-// (~200-300 cycles per CTA, tools/mb_tma.cu), so copies are kept few and big.
-// When an item covers whole z lines (NB*8 == Z) the z hops never leave the
-// item; otherwise the z-edge sites are read with ordinary loads.
-template <typename R, int V, int B, int NB_> struct RingShape {
-  static constexpr int BT = B / V;                       // threads per site
-  static constexpr int NB = NB_;                         // site blocks per item
-  static constexpr int NC = BT * 8 * NB;                 // consumer threads
-  static constexpr int NCW = NC / 32;                    // consumer warps
-  static constexpr int NT = NC + 32;                     // + producer warp
-  static constexpr int SPIN = NB * 96 * B;               // complex per spinor tile
-  static constexpr int SLOT = SPIN + NB * 72;            // + one link direction per block
-  static constexpr int SLOT_BYTES = SLOT * (int)sizeof(cx<R>);
-  static constexpr bool valid = (NC % 32 == 0) && NC >= 64 && NC <= 256 && (size_t)SLOT_BYTES * 2 <= 220 * 1024;
-  static size_t smem(int S) { return (size_t)SLOT_BYTES * S + 16 * S; }
-};
-
-// Coordinates of the first site of a site block (32-bit arithmetic: a rank's
-// local lattice has < 2^31 sites).
-struct BlkCoord {
-  int t, x, y, z0;
-};
-__device__ __forceinline__ BlkCoord block_coord(int64_t g, const HopParams& p) {
-  uint32_t s0 = (uint32_t)(g * 8);
-  BlkCoord c;
-  c.z0 = (int)(s0 % (uint32_t)p.Z);
-  s0 /= (uint32_t)p.Z;
-  c.y = (int)(s0 % (uint32_t)p.Y);
-  s0 /= (uint32_t)p.Y;
-  c.x = (int)(s0 % (uint32_t)p.X);
-  c.t = (int)(s0 / (uint32_t)p.X);
-  return c;
-}
-__device__ __forceinline__ void block_step(BlkCoord& c, const HopParams& p) {
-  c.z0 += 8;
-  if (c.z0 == p.Z) {
-    c.z0 = 0;
-    if (++c.y == p.Y) {
-      c.y = 0;
-      if (++c.x == p.X) {
-        c.x = 0;
-        ++c.t;
-      }
-    }
-  }
-}
-template <int MU, bool FWD>
-__device__ __forceinline__ int64_t block_neighbor(int64_t g, const BlkCoord& c, const HopParams& p) {
-  const int64_t s0 = g * 8;
-  const int64_t sY = p.Z, sX = (int64_t)p.Y * p.Z, sT = p.per_t;
-  int64_t ns;
-  if constexpr (MU == 0) ns = FWD ? (c.t + 1 == p.T ? s0 - (int64_t)(p.T - 1) * sT : s0 + sT)
-                                  : (c.t == 0 ? s0 + (int64_t)(p.T - 1) * sT : s0 - sT);
-  else if constexpr (MU == 1) ns = FWD ? (c.x + 1 == p.X ? s0 - (int64_t)(p.X - 1) * sX : s0 + sX)
-                                       : (c.x == 0 ? s0 + (int64_t)(p.X - 1) * sX : s0 - sX);
-  else ns = FWD ? (c.y + 1 == p.Y ? s0 - (int64_t)(p.Y - 1) * sY : s0 + sY)
-                : (c.y == 0 ? s0 + (int64_t)(p.Y - 1) * sY : s0 - sY);
-  return ns >> 3;
-}
-__device__ __forceinline__ int64_t z_neighbor(int64_t d, int z, int Z, int step) {
-  if (step > 0) return (z + 1 == Z) ? d - (Z - 1) : d + 1;
-  return (z == 0) ? d + (Z - 1) : d - 1;
-}
-
-// tile H in 0..5: hop (mu = H/2, forward if H even); H == 6: own blocks (z tile)
-template <typename R, int V, int B, int NB, int H>
-__device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, const BlkCoord& c0, cx<R>* slot,
-                                           uint64_t* full) {
-  using C = cx<R>;
-  using Sh = RingShape<R, V, B, NB>;
-  const C* src = static_cast<const C*>(p.src);
-  const C* U = static_cast<const C*>(p.U);
-  const int64_t nblk = p.n >> 3;
-  mbar_expect_tx(full, (uint32_t)(Sh::SLOT * sizeof(C)));
-  if constexpr (H == 6) {
-    bulk_g2s(slot, src + gb0 * 96 * B, Sh::SPIN * sizeof(C), full);
-    bulk_g2s(slot + Sh::SPIN, U + (3 * nblk + gb0) * 72, NB * 72 * sizeof(C), full);
-  } else {
-    constexpr int MU = H >> 1;
-    constexpr bool FWD = !(H & 1);
-    // neighbour blocks of the NB own blocks: contiguous unless a wrap falls inside the item
-    const int64_t nb0 = block_neighbor<MU, FWD>(gb0, c0, p);
-    bool contiguous = true;
-    if constexpr (NB > 1) {
-      BlkCoord c = c0;
-#pragma unroll
-      for (int jj = 1; jj < NB; ++jj) {
-        block_step(c, p);
-        contiguous &= block_neighbor<MU, FWD>(gb0 + jj, c, p) == nb0 + jj;
-      }
-    }
-    if (contiguous) {
-      bulk_g2s(slot, src + nb0 * 96 * B, Sh::SPIN * sizeof(C), full);
-      bulk_g2s(slot + Sh::SPIN, U + (MU * nblk + (FWD ? gb0 : nb0)) * 72, NB * 72 * sizeof(C), full);
-    } else {
-      BlkCoord c = c0;
-#pragma unroll
-      for (int jj = 0; jj < NB; ++jj) {
-        if (jj) block_step(c, p);
-        const int64_t nb = block_neighbor<MU, FWD>(gb0 + jj, c, p);
-        bulk_g2s(slot + jj * 96 * B, src + nb * 96 * B, 96 * B * sizeof(C), full);
-        bulk_g2s(slot + Sh::SPIN + jj * 72, U + (MU * nblk + (FWD ? gb0 + jj : nb)) * 72, 72 * sizeof(C), full);
-      }
-    }
-  }
-}
-
-template <typename R, int V, int B, int NB>
-__global__ void __launch_bounds__(RingShape<R, V, B, NB>::NT) hop_ring_kernel(const HopParams p, int64_t n_items,
-                                                                              int S) {
-  using C = cx<R>;
-  using Sh = RingShape<R, V, B, NB>;
-  constexpr int KST = 8 * B;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  C* ring = reinterpret_cast<C*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + S * Sh::SLOT);
-  uint64_t* empty = full + S;
-
-  const int tid = threadIdx.x;  // 1-D block: consumers [0, NC), producer warp [NC, NC+32)
-  if (tid == 0) {
-    for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], Sh::NCW);
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
-
-  if (tid >= Sh::NC) {
-    if (tid == Sh::NC) {  // one elected lane issues every copy
-      int pslot = 0, pfirst = 1;
-      uint32_t pphase = 0;  // phase of the next fill of pslot; its release is phase^1 of empty
-      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int64_t gb0 = (p.d_begin >> 3) + it * NB;
-        const BlkCoord c0 = block_coord(gb0, p);
-#define B200WD_PRODUCE(H)                                                    \
-  {                                                                          \
-    if (pfirst == 0) mbar_wait(&empty[pslot], pphase ^ 1u);                  \
-    ring_issue<R, V, B, NB, H>(p, gb0, c0, ring + pslot * Sh::SLOT, &full[pslot]); \
-    if (++pslot == S) {                                                      \
-      pslot = 0;                                                             \
-      pphase ^= 1u;                                                          \
-      pfirst = 0;                                                            \
-    }                                                                        \
-  }
-        B200WD_PRODUCE(6)
-        B200WD_PRODUCE(0)
-        B200WD_PRODUCE(1)
-        B200WD_PRODUCE(2)
-        B200WD_PRODUCE(3)
-        B200WD_PRODUCE(4)
-        B200WD_PRODUCE(5)
-#undef B200WD_PRODUCE
-      }
-    }
-    return;
-  }
-
-  // ---- consumers ----
-  const int r0 = (tid % Sh::BT) * V;
-  const int ysite = tid / Sh::BT;
-  const int j = ysite >> 3, lo = ysite & 7;
-  const bool lead = (tid & 31) == 0;
-  const C* __restrict__ src = static_cast<const C*>(p.src);
-  const C* __restrict__ U = static_cast<const C*>(p.U);
-  const int64_t nblk = p.n >> 3;
-  const int Z = p.Z;
-  R scb[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) scb[v] = (p.scale ? R(__ldg(p.scale + r0 + v)) : R(1)) * R(p.beta);
-  // acc accumulates (alpha/beta) xself + 2H src; out = (scale beta) acc
-  const R ab = (p.xself != nullptr) ? R(p.alpha / p.beta) : R(0);
-  const bool self_is_src = p.xself == p.src;
-
-  int cslot = 0;
-  uint32_t cphase = 0;
-  for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
-    const int64_t gb0 = (p.d_begin >> 3) + it * NB;
-    const int64_t d = (gb0 + j) * 8 + lo;
-    C acc[V][12];
-    {  // own blocks: xself, z hops
-      const int slot = cslot;
-      mbar_wait(&full[slot], cphase);
-      const C* zt = ring + slot * Sh::SLOT;
-      if (self_is_src || p.xself) {
-        const C* xp = self_is_src ? zt + j * 96 * B + lo * B + r0
-                                  : static_cast<const C*>(p.xself) + spinor_base(d, 12, B) + r0;
-#pragma unroll
-        for (int k = 0; k < 12; ++k) {
-          C xv[V];
-          if (self_is_src) VecIO<R, V>::lds(xv, xp + k * KST);
-          else VecIO<R, V>::ld(xv, xp + k * KST);
-#pragma unroll
-          for (int v = 0; v < V; ++v) acc[v][k] = mk(ab * xv[v].x, ab * xv[v].y);
-        }
-      } else {
-#pragma unroll
-        for (int v = 0; v < V; ++v)
-#pragma unroll
-          for (int k = 0; k < 12; ++k) acc[v][k] = mk(R(0), R(0));
-      }
-      const int z = (int)((uint32_t)d % (uint32_t)Z);
-      {
-        const int64_t nd = z_neighbor(d, z, Z, 1);
-        const int64_t jb = (nd >> 3) - gb0;
-        const C* ul = zt + Sh::SPIN + j * 72 + lo;  // U_3(x), own blocks
-        if (jb >= 0 && jb < NB)
-          hop_full<3, true, R, V, true, true>(acc, zt + jb * 96 * B + (nd & 7) * B + r0, KST, ul, 8);
-        else
-          hop_full<3, true, R, V, false, true>(acc, src + spinor_base(nd, 12, B) + r0, KST, ul, 8);
-      }
-      {
-        const int64_t nd = z_neighbor(d, z, Z, -1);
-        const int64_t jb = (nd >> 3) - gb0;
-        if (jb >= 0 && jb < NB)
-          hop_full<3, false, R, V, true, true>(acc, zt + jb * 96 * B + (nd & 7) * B + r0, KST,
-                                               zt + Sh::SPIN + jb * 72 + (nd & 7), 8);
-        else
-          hop_full<3, false, R, V, false, false>(acc, src + spinor_base(nd, 12, B) + r0, KST,
-                                                 U + link_base(nd, 3, nblk), 8);
-      }
-      __syncwarp();
-      if (lead) mbar_arrive(&empty[slot]);
-      if (++cslot == S) {
-        cslot = 0;
-        cphase ^= 1u;
-      }
-    }
-
-#define B200WD_CONSUME(H)                                                                            \
-  {                                                                                                  \
-    const int slot = cslot;                                                                          \
-    mbar_wait(&full[slot], cphase);                                                                  \
-    const C* sb = ring + slot * Sh::SLOT;                                                            \
-    if (!B200WD_RING_NOMATH)                                                                         \
-      hop_full<((H) >> 1), !((H)&1), R, V, true, true>(acc, sb + j * 96 * B + lo * B + r0, KST,      \
-                                                        sb + Sh::SPIN + j * 72 + lo, 8);             \
-    __syncwarp();                                                                                    \
-    if (lead) mbar_arrive(&empty[slot]);                                                             \
-    if (++cslot == S) {                                                                              \
-      cslot = 0;                                                                                     \
-      cphase ^= 1u;                                                                                  \
-    }                                                                                                \
-  }
-    B200WD_CONSUME(0)
-    B200WD_CONSUME(1)
-    B200WD_CONSUME(2)
-    B200WD_CONSUME(3)
-    B200WD_CONSUME(4)
-    B200WD_CONSUME(5)
-#undef B200WD_CONSUME
-
-    C* out = static_cast<C*>(p.out) + spinor_base(d, 12, B) + r0;
-#pragma unroll
-    for (int k = 0; k < 12; ++k) {
-      C res[V];
-#pragma unroll
-      for (int v = 0; v < V; ++v) res[v] = mk(scb[v] * acc[v][k].x, scb[v] * acc[v][k].y);
-      VecIO<R, V>::st(out + k * KST, res);
-    }
-  }
-}
-
-static int g_sm_count = 0;
-
-// Ring configuration: site blocks per item (compile time) and ring depth
-// (runtime).  Default: whole z lines per item when that gives <= 256
-// consumer threads, a ring of ~100 KB per CTA (two CTAs per SM) or ~200 KB
-// (one CTA) for large slots; B200WD_RING_CFG="NB,S" overrides (tuning).
-struct RingCfg {
-  int nb = 0, s = 0;
-};
-static RingCfg ring_env() {
-  static RingCfg c{-1, -1};
-  if (c.nb < 0) {
-    c = RingCfg{};
-    const char* e = getenv("B200WD_RING_CFG");
-    if (e) sscanf(e, "%d,%d", &c.nb, &c.s);
-  }
-  return c;
-}
-
-template <typename R, int V, int B, int NB>
-static bool launch_ring_nb(const HopParams& p, int64_t nblk, int S, cudaStream_t st) {
-  using Sh = RingShape<R, V, B, NB>;
-  if constexpr (!Sh::valid) {
-    return false;
-  } else {
-    if (nblk % NB) return false;
-    if (S <= 0) S = (Sh::SLOT_BYTES >= 40 * 1024) ? (200 * 1024) / Sh::SLOT_BYTES : (100 * 1024) / Sh::SLOT_BYTES;
-    if (S < 2) S = 2;
-    if (S > 8) S = 8;
-    const size_t smem = Sh::smem(S);
-    static size_t attr_smem = 0;
-    if (attr_smem < smem) {
-      if (cudaFuncSetAttribute(hop_ring_kernel<R, V, B, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem) != cudaSuccess)
-        return false;
-      attr_smem = smem;
-    }
-    int ctas_per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, hop_ring_kernel<R, V, B, NB>, Sh::NT, smem) !=
-            cudaSuccess ||
-        ctas_per_sm <= 0)
-      return false;
-    static int sm_count = 0;
-    if (sm_count == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const int64_t n_items = nblk / NB;
-    int64_t grid = (int64_t)ctas_per_sm * sm_count;
-    if (grid > n_items) grid = n_items;
-    hop_ring_kernel<R, V, B, NB><<<(unsigned)grid, Sh::NT, smem, st>>>(p, n_items, S);
-    return true;
-  }
-}
-
-// Measured best (NB, S) per (dtype, b) (tools/tune_ring.py on B200); {0,0}
-// = defaults (whole z lines per item, ~100/200 KB ring).
-template <typename R, int V, int B>
-static RingCfg ring_table(int Z) {
-  (void)Z;
-  if constexpr (sizeof(R) == 8) {
-    switch (B) {
-      case 4: return RingCfg{2, 3};
-      case 6: return RingCfg{2, 3};
-      case 8: return RingCfg{2, 4};
-      case 12: return RingCfg{2, 4};
-      case 16: return RingCfg{2, 4};
-      case 24: return RingCfg{1, 6};
-      case 32: return RingCfg{2, 6};
-      default: return RingCfg{};
-    }
-  } else {
-    switch (B) {
-      case 4: return RingCfg{4, 3};
-      case 6: return RingCfg{4, 2};
-      case 8: return RingCfg{2, 4};
-      case 12: return RingCfg{2, 2};
-      case 16: return RingCfg{2, 2};
-      case 24: return RingCfg{1, 3};
-      case 32: return RingCfg{2, 4};
-      default: return RingCfg{};
-    }
-  }
-}
-
-// Launch the ring kernel when its shape preconditions hold (full lattice, no
-// halos, Z % 8 == 0); false -> the caller uses the generic kernel.
-template <typename R, int V, int B>
-static bool try_launch_ring(const HopParams& p, cudaStream_t st) {
-  if (p.dst_parity >= 0 || p.lam_halo != nullptr || p.Z % 8 != 0 || p.beta == 0.0) return false;
-  if ((p.d_begin & 7) || (p.d_end & 7)) return false;
-  const int64_t nblk = (p.d_end - p.d_begin) >> 3;
-  const RingCfg env = ring_env();
-  RingCfg c = ring_table<R, V, B>(p.Z);
-  if (env.nb > 0) c.nb = env.nb;
-  if (env.s > 0) c.s = env.s;
-  if (c.nb <= 0) c.nb = p.Z / 8;  // whole z lines per item
-  switch (c.nb) {
-    case 4:
-      if (launch_ring_nb<R, V, B, 4>(p, nblk, c.s, st)) return true;
-      break;
-    case 2:
-      if (launch_ring_nb<R, V, B, 2>(p, nblk, c.s, st)) return true;
-      break;
-    case 1:
-      if (launch_ring_nb<R, V, B, 1>(p, nblk, c.s, st)) return true;
-      break;
-    default:
-      break;
-  }
-  // partial lines: the z edges use ordinary loads
-  if (launch_ring_nb<R, V, B, 2>(p, nblk, 0, st)) return true;
-  return launch_ring_nb<R, V, B, 1>(p, nblk, 0, st);
-}
-
-// ---- halo face pack (halo.py:352-368) ---------------------------------------
-template <typename R, int V>
-__global__ void __launch_bounds__(256) halo_pack_kernel(const HopParams p, void* lam_face, void* chi_face) {
-  using C = cx<R>;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;  // face index
-  if (i >= p.nf) return;
-  const int r0 = threadIdx.x * V;
-  const int b = p.b;
-  const bool par = p.dst_parity >= 0;  // parity of the source field
-  const C* __restrict__ src = static_cast<const C*>(p.src);
-  const C* __restrict__ U = static_cast<const C*>(p.U);
-  const int kst = 8 * b;
-  const int64_t fstride = p.nf * b;
-  for (int face = 0; face < 2; ++face) {
-    const int tf = face == 0 ? 0 : p.T - 1;
-    const int64_t sidx = par ? i + (int64_t)tf * (p.per_t / 2) : i + (int64_t)tf * p.per_t;
-    int64_t site = sidx;
-    if (par) {
-      site = 2 * sidx;
-      const int z = (int)(site % p.Z);
-      int64_t q = site / p.Z;
-      const int y = (int)(q % p.Y);
-      q /= p.Y;
-      const int x = (int)(q % p.X);
-      const int t = (int)(q / p.X);
-      site += (t + x + y + z + p.par0 + p.dst_parity) & 1;
-    }
-    const C* sp = src + spinor_base(sidx, 12, b) + r0;
-    C psi[V][12];
-#pragma unroll
-    for (int k = 0; k < 12; ++k) {
-      C tmp[V];
-      VecIO<R, V>::ld(tmp, sp + k * kst);
-#pragma unroll
-      for (int v = 0; v < V; ++v) psi[v][k] = tmp[v];
-    }
-    if (face == 0) {
-      C* out = static_cast<C*>(lam_face) + i * b + r0;
-#pragma unroll
-      for (int hk = 0; hk < 6; ++hk) {
-        C res[V];
-#pragma unroll
-        for (int v = 0; v < V; ++v) res[v] = cadd(psi[v][hk], psi[v][6 + hk]);  // u + A_0 l
-        VecIO<R, V>::st(out + hk * fstride, res);
-      }
-    } else {
-      const C* ux = U + link_base(site, 0, p.n >> 3);
-      C u[9];
-#pragma unroll
-      for (int e = 0; e < 9; ++e) u[e] = __ldg(ux + e * 8);
-      C g[V][2][3];
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        C h[2][3];
-        project_spin<0, false, 0>(h[0], psi[v]);
-        project_spin<0, false, 1>(h[1], psi[v]);
-        matvec2<true>(g[v], u, h);
-      }
-      C* out = static_cast<C*>(chi_face) + i * b + r0;
-#pragma unroll
-      for (int hk = 0; hk < 6; ++hk) {
-        C res[V];
-#pragma unroll
-        for (int v = 0; v < V; ++v) res[v] = g[v][hk / 3][hk % 3];
-        VecIO<R, V>::st(out + hk * fstride, res);
-      }
-    }
-  }
-}
-
-static bool bulk_enabled() {
-  static int en = -1;
-  if (en < 0) {
-    const char* e = getenv("B200WD_NO_TMA");
-    en = (e && e[0] == '1') ? 0 : 1;
-  }
-  return en == 1;
-}
-
-template <typename R, int V, int B>
-static void launch_hop_b(const HopParams& p, cudaStream_t st) {
-  if constexpr (B >= 4) {
-    if (bulk_enabled() && try_launch_ring<R, V, B>(p, st)) return;
-  }
-  const int bt = (B > 0 ? B : p.b) / V;
-  const int S = bt >= kHopThreads ? 1 : kHopThreads / bt;
-  dim3 block(bt, S);
-  const int64_t nd = p.d_end - p.d_begin;
-  dim3 grid((unsigned)((nd + S - 1) / S));
-  hop_kernel<R, V, B><<<grid, block, 0, st>>>(p);
-}
-
-// compile-time rhs counts that get their own instantiation per (R, V)
-template <typename R, int V> __host__ __device__ constexpr bool wanted_b(int bb) {
-  return bb % V == 0 && (V == 2 || sizeof(R) == 8 || bb % 2 == 1);
-}
-
-template <typename R, int V>
-static void launch_hop(const HopParams& p, cudaStream_t st) {
-  switch (p.b) {
-#define B200WD_CASE(BB)                       \
-  case BB:                                    \
-    if constexpr (wanted_b<R, V>(BB)) {       \
-      launch_hop_b<R, V, BB>(p, st);          \
-      return;                                 \
-    }                                         \
-    break;
-    B200WD_CASE(1)
-    B200WD_CASE(2)
-    B200WD_CASE(3)
-    B200WD_CASE(4)
-    B200WD_CASE(6)
-    B200WD_CASE(8)
-    B200WD_CASE(12)
-    B200WD_CASE(16)
-    B200WD_CASE(24)
-    B200WD_CASE(32)
-#undef B200WD_CASE
-    default:
-      break;
-  }
-  launch_hop_b<R, V, 0>(p, st);
-}
-
-template <typename R, int V>
-static void launch_pack(const HopParams& p, void* lam, void* chi, cudaStream_t st) {
-  const int bt = p.b / V;
-  const int S = bt >= 256 ? 1 : 256 / bt;
-  dim3 block(bt, S);
-  dim3 grid((unsigned)((p.nf + S - 1) / S));
-  halo_pack_kernel<R, V><<<grid, block, 0, st>>>(p, lam, chi);
-}
 
 static int fill_params(HopParams& p, const b200wd_lattice* lat, int32_t dtype, int32_t b, int32_t parity) {
   B200WD_REQUIRE(lat != nullptr, "lattice descriptor is NULL");
@@ -726,13 +71,8 @@ extern "C" int b200wd_hop(const b200wd_lattice* lat, int32_t dtype, int32_t b, i
   p.d_begin = per * t_begin;
   p.d_end = per * t_end;
   cudaStream_t st = as_stream(stream);
-  if (dtype == B200WD_C128) {
-    launch_hop<double, 1>(p, st);
-  } else if (b % 2 == 0) {
-    launch_hop<float, 2>(p, st);
-  } else {
-    launch_hop<float, 1>(p, st);
-  }
+  if (dtype == B200WD_C128) launch_hop_c128(p, st);
+  else launch_hop_c64(p, st);
   return check_launch("b200wd_hop");
 }
 
@@ -752,8 +92,7 @@ extern "C" int b200wd_halo_pack(const b200wd_lattice* lat, int32_t dtype, int32_
   p.U = links;
   p.src = src;
   cudaStream_t st = as_stream(stream);
-  if (dtype == B200WD_C128) launch_pack<double, 1>(p, lam_face, chi_face, st);
-  else if (b % 2 == 0) launch_pack<float, 2>(p, lam_face, chi_face, st);
-  else launch_pack<float, 1>(p, lam_face, chi_face, st);
+  if (dtype == B200WD_C128) launch_pack_c128(p, lam_face, chi_face, st);
+  else launch_pack_c64(p, lam_face, chi_face, st);
   return check_launch("b200wd_halo_pack");
 }
