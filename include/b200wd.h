@@ -79,6 +79,11 @@ int b200wd_spinor_export(const void* src, int32_t dtype, int64_t n_sites, int32_
  * device link planes of `dtype`. */
 int b200wd_gauge_import(const void* src_c128, int64_t n_sites, void* dst, int32_t dtype,
                         void* stream);
+/* CloverField.data (n,2,21) complex128 packed blocks (fields.py:212-247) ->
+ * device site-blocked blocks: element (site, q) at ((site>>3)*42 + q)*8 +
+ * (site&7).  Also used for the packed inverse blocks of the Schur operator. */
+int b200wd_clover_import(const void* src_c128, int64_t n_sites, void* dst, int32_t dtype,
+                         void* stream);
 /* Full-lattice planes <-> (even, odd) parity planes; replaces split_fields /
  * merge_fields (oddeven.py:72-95). */
 int b200wd_parity_split(const b200wd_lattice* lat, int32_t dtype, int32_t s, int32_t b,
@@ -105,6 +110,23 @@ int b200wd_hop(const b200wd_lattice* lat, int32_t dtype, int32_t b, int32_t dst_
                const void* links, const void* src, const void* xself, void* out, double alpha,
                double beta, const double* scale, int32_t t_begin, int32_t t_end,
                const void* lam_halo, const void* chi_halo, void* stream);
+
+/* b200wd_hop plus a site-local term (the clover, dirac.py:137-157, or the
+ * inverse of the eliminated diagonal blocks, oddeven.py:123-144): `clover`
+ * holds two packed Hermitian 6x6 blocks (21 complex each, lower triangle
+ * row-major as CloverField.data, fields.py:212-247) per dst site, imported
+ * with b200wd_clover_import.
+ *   clover_mode 0: as b200wd_hop
+ *   clover_mode 1: out = scale (alpha xself - M xself + beta H src)
+ *   clover_mode 2: out = scale  M (alpha xself + beta H src)              */
+int b200wd_hop_clover(const b200wd_lattice* lat, int32_t dtype, int32_t b, int32_t dst_parity,
+                      const void* links, const void* src, const void* xself, void* out, double alpha,
+                      double beta, const double* scale, int32_t t_begin, int32_t t_end,
+                      const void* lam_halo, const void* chi_halo, const void* clover,
+                      int32_t clover_mode, void* stream);
+/* out = M x, site-local (D_oo^-1 eta_o of reduce_rhs, oddeven.py:179-188). */
+int b200wd_clover_apply(int64_t n_sites, int32_t dtype, int32_t b, const void* blocks,
+                        const void* x, void* out, void* stream);
 
 /* eta = D psi = (4+m0) psi - H psi on the full (single-rank) lattice with
  * C = 0; replaces apply_dirac (dirac.py:299-334). */

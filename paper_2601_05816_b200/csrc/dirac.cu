@@ -76,6 +76,52 @@ extern "C" int b200wd_hop(const b200wd_lattice* lat, int32_t dtype, int32_t b, i
   return check_launch("b200wd_hop");
 }
 
+extern "C" int b200wd_hop_clover(const b200wd_lattice* lat, int32_t dtype, int32_t b, int32_t dst_parity,
+                                 const void* links, const void* src, const void* xself, void* out, double alpha,
+                                 double beta, const double* scale, int32_t t_begin, int32_t t_end,
+                                 const void* lam_halo, const void* chi_halo, const void* clover, int32_t clover_mode,
+                                 void* stream) {
+  HopParams p;
+  if (int rc = fill_params(p, lat, dtype, b, dst_parity)) return rc;
+  B200WD_REQUIRE(links && src && out, "NULL field pointer");
+  B200WD_REQUIRE(clover_mode >= 0 && clover_mode <= 2, "clover_mode must be 0, 1 or 2 (got %d)", clover_mode);
+  B200WD_REQUIRE(clover_mode == 0 || clover != nullptr, "clover_mode %d needs a clover array", clover_mode);
+  B200WD_REQUIRE(0 <= t_begin && t_begin <= t_end && t_end <= p.T, "slice range [%d,%d) outside [0,%d)", t_begin,
+                 t_end, p.T);
+  B200WD_REQUIRE((lam_halo == nullptr) == (chi_halo == nullptr), "lam_halo and chi_halo must both be set or NULL");
+  if (t_begin == t_end) return B200WD_OK;
+  p.U = links;
+  p.src = src;
+  p.xself = xself;
+  p.out = out;
+  p.alpha = alpha;
+  p.beta = 0.5 * beta;
+  p.scale = scale;
+  p.lam_halo = lam_halo;
+  p.chi_halo = chi_halo;
+  p.clov = clover;
+  p.clov_mode = clover_mode;
+  const int64_t per = dst_parity < 0 ? p.per_t : p.per_t / 2;
+  p.d_begin = per * t_begin;
+  p.d_end = per * t_end;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == B200WD_C128) launch_hop_c128(p, st);
+  else launch_hop_c64(p, st);
+  return check_launch("b200wd_hop_clover");
+}
+
+extern "C" int b200wd_clover_apply(int64_t n_sites, int32_t dtype, int32_t b, const void* blocks, const void* x,
+                                   void* out, void* stream) {
+  B200WD_REQUIRE(n_sites >= 8 && n_sites % 8 == 0, "site count %lld must be a positive multiple of 8",
+                 (long long)n_sites);
+  B200WD_REQUIRE(b >= 1 && blocks && x && out, "bad clover_apply arguments");
+  cudaStream_t st = as_stream(stream);
+  if (dtype == B200WD_C128) launch_clover_apply_c128(n_sites, b, blocks, x, out, st);
+  else if (dtype == B200WD_C64) launch_clover_apply_c64(n_sites, b, blocks, x, out, st);
+  else B200WD_REQUIRE(false, "unknown dtype %d", dtype);
+  return check_launch("b200wd_clover_apply");
+}
+
 extern "C" int b200wd_dirac_apply(const b200wd_lattice* lat, int32_t dtype, int32_t b, double m0,
                                   const void* links, const void* psi, void* eta, void* stream) {
   B200WD_REQUIRE(lat != nullptr, "lattice descriptor is NULL");

@@ -25,6 +25,9 @@
 
 namespace b200wd {
 
+#ifndef B200WD_PAIR_HOPS
+#define B200WD_PAIR_HOPS 0  // 1: consume the two tiles of one direction together (measured slower)
+#endif
 #ifndef B200WD_RING_NOMATH
 #define B200WD_RING_NOMATH 0  // experiment: consumers skip the t/x/y arithmetic
 #endif
@@ -131,6 +134,45 @@ __global__ void __launch_bounds__(kHopThreads, HopMinBlocks<R>::value) hop_kerne
 #pragma unroll
   for (int v = 0; v < V; ++v) sc[v] = p.scale ? R(__ldg(p.scale + r0 + v)) : R(1);
   const R beta = R(p.beta), alpha = R(p.alpha);
+  if (p.clov_mode != 0) {  // site-local 12x12 block term (clover or its inverse)
+    const C* cl = static_cast<const C*>(p.clov) + clover_base(d);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      C x[12], t[12], y[12];
+#pragma unroll
+      for (int k = 0; k < 12; ++k) {
+        if (xs) {
+          C xv[V];
+          VecIO<R, V>::ld(xv, xs + k * kst);
+          x[k] = xv[v];
+        } else {
+          x[k] = mk(R(0), R(0));
+        }
+      }
+      if (p.clov_mode == 1) {
+        clover_mul(y, x, cl);
+#pragma unroll
+        for (int k = 0; k < 12; ++k)
+          acc[v][k] = mk(sc[v] * (alpha * x[k].x - y[k].x + beta * acc[v][k].x),
+                         sc[v] * (alpha * x[k].y - y[k].y + beta * acc[v][k].y));
+      } else {
+#pragma unroll
+        for (int k = 0; k < 12; ++k)
+          t[k] = mk(alpha * x[k].x + beta * acc[v][k].x, alpha * x[k].y + beta * acc[v][k].y);
+        clover_mul(y, t, cl);
+#pragma unroll
+        for (int k = 0; k < 12; ++k) acc[v][k] = mk(sc[v] * y[k].x, sc[v] * y[k].y);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+      C res[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) res[v] = acc[v][k];
+      VecIO<R, V>::st(out + k * kst, res);
+    }
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < 12; ++k) {
     C res[V];
@@ -392,6 +434,42 @@ __global__ void __launch_bounds__(RingShape<R, V, B, NB>::NT) hop_ring_kernel(co
       }
     }
 
+#if B200WD_PAIR_HOPS
+    // forward + backward tile of one direction together: two independent hops
+    // in one basic block give the scheduler twice the ILP
+#define B200WD_CONSUME_PAIR(H)                                                                        \
+  {                                                                                                  \
+    const int sa = cslot;                                                                            \
+    const uint32_t pa = cphase;                                                                      \
+    if (++cslot == S) {                                                                              \
+      cslot = 0;                                                                                     \
+      cphase ^= 1u;                                                                                  \
+    }                                                                                                \
+    const int sb_ = cslot;                                                                           \
+    const uint32_t pb = cphase;                                                                      \
+    if (++cslot == S) {                                                                              \
+      cslot = 0;                                                                                     \
+      cphase ^= 1u;                                                                                  \
+    }                                                                                                \
+    mbar_wait(&full[sa], pa);                                                                        \
+    mbar_wait(&full[sb_], pb);                                                                       \
+    const C* ta = ring + sa * Sh::SLOT;                                                              \
+    const C* tb = ring + sb_ * Sh::SLOT;                                                             \
+    hop_full<((H) >> 1), true, R, V, true, true>(acc, ta + j * 96 * B + lo * B + r0, KST,            \
+                                                 ta + Sh::SPIN + j * 72 + lo, 8);                    \
+    hop_full<((H) >> 1), false, R, V, true, true>(acc, tb + j * 96 * B + lo * B + r0, KST,           \
+                                                  tb + Sh::SPIN + j * 72 + lo, 8);                   \
+    __syncwarp();                                                                                    \
+    if (lead) {                                                                                      \
+      mbar_arrive(&empty[sa]);                                                                       \
+      mbar_arrive(&empty[sb_]);                                                                      \
+    }                                                                                                \
+  }
+    B200WD_CONSUME_PAIR(0)
+    B200WD_CONSUME_PAIR(2)
+    B200WD_CONSUME_PAIR(4)
+#undef B200WD_CONSUME_PAIR
+#else
 #define B200WD_CONSUME(H)                                                                            \
   {                                                                                                  \
     const int slot = cslot;                                                                          \
@@ -414,6 +492,7 @@ __global__ void __launch_bounds__(RingShape<R, V, B, NB>::NT) hop_ring_kernel(co
     B200WD_CONSUME(4)
     B200WD_CONSUME(5)
 #undef B200WD_CONSUME
+#endif
 
     C* out = static_cast<C*>(p.out) + spinor_base(d, 12, B) + r0;
 #pragma unroll
@@ -516,7 +595,8 @@ static RingCfg ring_table(int Z) {
 // halos, Z % 8 == 0); false -> the caller uses the generic kernel.
 template <typename R, int V, int B>
 static bool try_launch_ring(const HopParams& p, cudaStream_t st) {
-  if (p.dst_parity >= 0 || p.lam_halo != nullptr || p.Z % 8 != 0 || p.beta == 0.0) return false;
+  if (p.dst_parity >= 0 || p.lam_halo != nullptr || p.Z % 8 != 0 || p.beta == 0.0 || p.clov_mode != 0)
+    return false;
   if ((p.d_begin & 7) || (p.d_end & 7)) return false;
   const int64_t nblk = (p.d_end - p.d_begin) >> 3;
   const RingCfg env = ring_env();
@@ -540,6 +620,24 @@ static bool try_launch_ring(const HopParams& p, cudaStream_t st) {
   // partial lines: the z edges use ordinary loads
   if (launch_ring_nb<R, V, B, 2>(p, nblk, 0, st)) return true;
   return launch_ring_nb<R, V, B, 1>(p, nblk, 0, st);
+}
+
+// ---- site-local block apply: out = M x (D_oo^-1 eta_o of reduce_rhs) ---------
+template <typename R>
+__global__ void __launch_bounds__(256) clover_apply_kernel(int64_t n, int b, const cx<R>* __restrict__ M,
+                                                           const cx<R>* __restrict__ x, cx<R>* __restrict__ out) {
+  using C = cx<R>;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (site, r)
+  if (i >= n * b) return;
+  const int64_t site = i / b;
+  const int r = (int)(i % b);
+  const int64_t o = spinor_base(site, 12, b) + r;
+  C t[12], y[12];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) t[k] = __ldg(x + o + k * 8 * b);
+  clover_mul(y, t, M + clover_base(site));
+#pragma unroll
+  for (int k = 0; k < 12; ++k) out[o + k * 8 * b] = y[k];
 }
 
 // ---- halo face pack (halo.py:352-368) ---------------------------------------
@@ -680,5 +778,7 @@ void launch_hop_c128(const HopParams& p, cudaStream_t st);
 void launch_hop_c64(const HopParams& p, cudaStream_t st);
 void launch_pack_c128(const HopParams& p, void* lam, void* chi, cudaStream_t st);
 void launch_pack_c64(const HopParams& p, void* lam, void* chi, cudaStream_t st);
+void launch_clover_apply_c128(int64_t n, int b, const void* M, const void* x, void* out, cudaStream_t st);
+void launch_clover_apply_c64(int64_t n, int b, const void* M, const void* x, void* out, cudaStream_t st);
 
 }  // namespace b200wd

@@ -63,6 +63,20 @@ __global__ void gauge_import_kernel(const double2* __restrict__ in, C* __restric
   }
 }
 
+// (n, 2, 21) packed clover blocks -> site-blocked (layout.cuh clover_base)
+template <typename C>
+__global__ void clover_import_kernel(const double2* __restrict__ in, C* __restrict__ out, int64_t n) {
+  const int64_t total = n * 42;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int lo = (int)(i & 7);
+    const int64_t q = i >> 3;
+    const int e = (int)(q % 42);
+    const int64_t x = (q / 42) * 8 + lo;
+    out[i] = from_c128<C>(__ldg(in + x * 42 + e));
+  }
+}
+
 // full <-> parity fields; cb = site >> 1 (oddeven.py:62-65 ordering)
 template <typename C, bool SPLIT>
 __global__ void parity_kernel(C* __restrict__ full, C* __restrict__ even, C* __restrict__ odd, int64_t n, int s,
@@ -148,6 +162,21 @@ extern "C" int b200wd_gauge_import(const void* src_c128, int64_t n_sites, void* 
   else
     B200WD_REQUIRE(false, "unknown dtype %d", dtype);
   return check_launch("b200wd_gauge_import");
+}
+
+extern "C" int b200wd_clover_import(const void* src_c128, int64_t n_sites, void* dst, int32_t dtype, void* stream) {
+  B200WD_REQUIRE(n_sites >= 8 && n_sites % 8 == 0 && src_c128 && dst, "bad clover import arguments (n=%lld)",
+                 (long long)n_sites);
+  const int64_t total = n_sites * 42;
+  if (dtype == B200WD_C128)
+    clover_import_kernel<double2><<<grid_for(total), 256, 0, as_stream(stream)>>>(
+        static_cast<const double2*>(src_c128), static_cast<double2*>(dst), n_sites);
+  else if (dtype == B200WD_C64)
+    clover_import_kernel<float2><<<grid_for(total), 256, 0, as_stream(stream)>>>(
+        static_cast<const double2*>(src_c128), static_cast<float2*>(dst), n_sites);
+  else
+    B200WD_REQUIRE(false, "unknown dtype %d", dtype);
+  return check_launch("b200wd_clover_import");
 }
 
 static int parity_common(const b200wd_lattice* lat, int32_t dtype, int32_t s, int32_t b, void* full, void* even,

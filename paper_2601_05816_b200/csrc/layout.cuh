@@ -32,4 +32,8 @@ __host__ __device__ __forceinline__ int64_t link_base(int64_t site, int mu, int6
   return (mu * nblk + (site >> 3)) * 72 + (site & 7);
 }
 
+// Site-local clover blocks: 2 x 21 packed complex per site,
+//   element (site, q) at ((site >> 3) * 42 + q) * 8 + (site & 7),  q = 21*block + idx
+__host__ __device__ __forceinline__ int64_t clover_base(int64_t site) { return (site >> 3) * 336 + (site & 7); }
+
 }  // namespace b200wd

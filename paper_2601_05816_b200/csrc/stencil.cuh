@@ -35,7 +35,35 @@ struct HopParams {
   const double* scale;
   const void* lam_halo;
   const void* chi_halo;
+  // site-local term (clover, dirac.py:137-157): packed Hermitian 6x6 blocks,
+  // 2 x 21 complex per dst site (layout.cuh clover_base).  mode 1:
+  // out = s (alpha x - M x + beta H src); mode 2: out = s M (alpha x + beta H src)
+  const void* clov;
+  int32_t clov_mode;
 };
+
+// y = M t for the two packed Hermitian 6x6 blocks of one site (fields.py:212-247:
+// lower triangle, row-major, element (i,j), i >= j, at i(i+1)/2 + j)
+template <typename C>
+__device__ __forceinline__ void clover_mul(C (&y)[12], const C (&t)[12], const C* __restrict__ cl) {
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    C a[21];
+#pragma unroll
+    for (int e = 0; e < 21; ++e) a[e] = __ldg(cl + (q * 21 + e) * 8);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      C acc = mk(decltype(t[0].x)(0), decltype(t[0].x)(0));
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        const C m = i >= j ? a[i * (i + 1) / 2 + j] : cconj(a[j * (j + 1) / 2 + i]);
+        const C v = t[6 * q + j];
+        acc = mk(acc.x + m.x * v.x - m.y * v.y, acc.y + m.x * v.y + m.y * v.x);
+      }
+      y[6 * q + i] = acc;
+    }
+  }
+}
 
 // ---- V-wide loads/stores of consecutive rhs ---------------------------------
 template <typename R, int V> struct VecIO;

@@ -230,6 +230,32 @@ def upload_gauge(gauge, dtype: str = "c128", stream=None) -> DeviceGauge:
     return DeviceGauge(out, gauge.geom)
 
 
+@dataclass
+class DeviceClover:
+    """Packed Hermitian 6x6 block pairs (clover or inverse blocks) in HBM:
+    (n/8, 42, 8) site-blocked (csrc/layout.cuh clover_base)."""
+
+    data: "torch.Tensor"
+    n: int
+
+    @property
+    def ptr(self) -> int:
+        return int(self.data.data_ptr())
+
+
+def upload_packed_blocks(packed: np.ndarray, dtype: str = "c128", stream=None) -> DeviceClover:
+    """(n, 2, 21) complex128 packed blocks (CloverField.data layout) -> device."""
+    dev = require_device()
+    arr = np.ascontiguousarray(np.asarray(packed, dtype=np.complex128))
+    n = arr.shape[0]
+    if arr.shape != (n, 2, 21) or n % SITE_BLOCK:
+        raise ValueError(f"packed blocks have shape {arr.shape}; need (n, 2, 21) with n % 8 == 0")
+    raw = torch.from_numpy(arr.reshape(-1)).to(dev, non_blocking=True)
+    out = torch.empty((n // SITE_BLOCK, 42, SITE_BLOCK), dtype=torch_dtype(dtype), device=dev)
+    _lib.call("b200wd_clover_import", ptr(raw), n, ptr(out), dtype_code(dtype), stream_ptr(stream))
+    return DeviceClover(out, n)
+
+
 class _GaugeCache:
     """Upload each host GaugeField once per dtype.
 
@@ -250,15 +276,22 @@ class _GaugeCache:
     def get(self, gauge, dtype: str) -> DeviceGauge:
         if isinstance(gauge, DeviceGauge):
             return gauge
-        arr = gauge.data
-        key = (id(arr), dtype)
+        return self._get(gauge.data, dtype, "gauge", lambda: upload_gauge(gauge, dtype))
+
+    def get_clover(self, clover, dtype: str) -> DeviceClover:
+        if isinstance(clover, DeviceClover):
+            return clover
+        return self._get(clover.data, dtype, "clover", lambda: upload_packed_blocks(clover.data, dtype))
+
+    def _get(self, arr, dtype, kind, make):
+        key = (id(arr), dtype, kind)
         fp = self._fingerprint(arr)
         hit = self._entries.get(key)
         if hit is not None:
             ref, hfp, dg = hit
             if ref() is arr and hfp == fp:
                 return dg
-        dg = upload_gauge(gauge, dtype)
+        dg = make()
         try:
             ref = weakref.ref(arr)
         except TypeError:

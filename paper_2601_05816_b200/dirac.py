@@ -104,10 +104,15 @@ def _lattice(geom, t_origin: int = 0):
     return _lib.Lattice.make(geom.dims, t_origin)
 
 
+def clover_is_zero(clover) -> bool:
+    return clover is None or (clover.is_zero() if hasattr(clover, "is_zero") else not np.any(clover.data))
+
+
 def _check_clover(clover) -> None:
-    if clover is not None and not (clover.is_zero() if hasattr(clover, "is_zero") else not np.any(clover.data)):
-        raise NotImplementedError("the B200 path implements C = 0 (the BASELINE configurations); "
-                                  "a non-zero clover term is not supported by this build")
+    """Paths that implement C = 0 only (the multi-GPU T split) reject a clover term."""
+    if not clover_is_zero(clover):
+        raise NotImplementedError("this path implements C = 0 (the BASELINE multi-GPU configurations); "
+                                  "use the single-GPU operators for a non-zero clover term")
 
 
 class DiracOperator:
@@ -119,12 +124,13 @@ class DiracOperator:
     """
 
     def __init__(self, params: DiracParams, gauge, clover=None, dtype: str = "c128"):
-        _check_clover(clover)
         require_device()
         self.params = params
         self.dtype = dtype
         self.geom = gauge.geom
         self.gauge = gauge_cache.get(gauge, dtype)
+        # site-local clover term C (dirac.py:137-157): fused into the hop epilogue
+        self.clover = None if clover_is_zero(clover) else gauge_cache.get_clover(clover, dtype)
         self.lat = _lattice(self.geom)
         self.n_sites = self.geom.n_sites
         self.allreduce = None
@@ -136,8 +142,8 @@ class DiracOperator:
         if v.dtype != self.dtype:
             raise ValueError(f"field dtype {v.dtype} != operator dtype {self.dtype}")
         out = v.empty_like() if out is None else out
-        _lib.call("b200wd_hop", self.lat, dtype_code(self.dtype), v.b, -1, self.gauge.ptr, v.ptr, v.ptr, out.ptr,
-                  4.0 + self.params.m0, -1.0, ptr(scale), 0, self.geom.dims[0], None, None, stream_ptr(stream))
+        hop_device(self.lat, self.dtype, v.b, -1, self.gauge, v, out, v, 4.0 + self.params.m0, -1.0, scale,
+                   clover=self.clover, clover_mode=1, stream=stream)
         return out
 
     def __call__(self, v):
@@ -187,9 +193,13 @@ def apply_dirac(params: DiracParams, gauge, clover, psi, comm=None, flops: FlopC
 
 def hop_device(lat, dtype: str, b: int, dst_parity: int, gauge: DeviceGauge, src: DeviceField, out: DeviceField,
                xself: DeviceField | None, alpha: float, beta: float, scale=None, t_begin: int = 0,
-               t_end: int | None = None, lam_halo=None, chi_halo=None, stream=None) -> None:
-    """Thin wrapper over ``b200wd_hop`` (see include/b200wd.h)."""
+               t_end: int | None = None, lam_halo=None, chi_halo=None, stream=None, clover=None,
+               clover_mode: int = 0) -> None:
+    """Thin wrapper over ``b200wd_hop`` / ``b200wd_hop_clover`` (include/b200wd.h)."""
     t_end = lat.dims[0] if t_end is None else t_end
-    _lib.call("b200wd_hop", lat, dtype_code(dtype), b, dst_parity, gauge.ptr, src.ptr,
-              None if xself is None else xself.ptr, out.ptr, float(alpha), float(beta), ptr(scale),
-              int(t_begin), int(t_end), ptr(lam_halo), ptr(chi_halo), stream_ptr(stream))
+    args = (lat, dtype_code(dtype), b, dst_parity, gauge.ptr, src.ptr, None if xself is None else xself.ptr,
+            out.ptr, float(alpha), float(beta), ptr(scale), int(t_begin), int(t_end), ptr(lam_halo), ptr(chi_halo))
+    if clover is None or clover_mode == 0:
+        _lib.call("b200wd_hop", *args, stream_ptr(stream))
+    else:
+        _lib.call("b200wd_hop_clover", *args, clover.ptr, int(clover_mode), stream_ptr(stream))

@@ -7,6 +7,9 @@ With C = 0 the site-local blocks are (4+m0) I, so with H the hopping sum
     reduce_rhs : eta~_e = eta_e + H_eo eta_o / (4+m0)
     reconstruct: x_o    = (eta_o + H_oe x_e) / (4+m0)
 
+With a clover term the eliminated blocks (4+m0) I - C are inverted once on
+the host with the reference's condition check and applied in the kernel
+epilogue (clover_mode 2); the kept blocks are applied as -C v (mode 1).
 Each line is one or two launches of the parity-restricted fused hopping
 kernel (``b200wd_hop`` with dst_parity = 0/1); the reference instead embeds
 the half field in the full lattice and hops every site twice per apply
@@ -20,8 +23,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .device import DeviceField, dtype_code, gauge_cache, require_device, stream_ptr, upload
-from .dirac import DiracParams, _check_clover, _lattice, hop_device
+from .device import DeviceField, dtype_code, gauge_cache, ptr, require_device, stream_ptr, upload, upload_packed_blocks
+from .dirac import DiracParams, _lattice, clover_is_zero, hop_device
 from .fields import SPINOR_LEN, BlockSpinorField, Layout
 from .geometry import LatticeGeometry
 
@@ -106,7 +109,6 @@ class SchurOperator:
                  dtype: str = "c128", lattice=None, gauge_dev=None, comm=None):
         if keep_parity not in (0, 1):
             raise ValueError(f"parity must be 0 (even) or 1 (odd), got {keep_parity}")
-        _check_clover(clover)
         self.params = params
         self.keep_parity = keep_parity
         self.elim_parity = 1 - keep_parity
@@ -116,10 +118,27 @@ class SchurOperator:
         # diagonal blocks of the eliminated parity are (4+m0) I (C = 0):
         # condition number 1, or infinite when 4+m0 = 0 (oddeven.py:123-132)
         self.diag = 4.0 + params.m0
-        if self.diag == 0.0 or not np.isfinite(self.diag):
-            elim = self.geom.odd_sites if keep_parity == 0 else self.geom.even_sites
-            raise SingularBlockError(int(elim[0]), 0, float("inf"))
+        self.clover_inv = self.clover_keep = None
+        elim = self.geom.odd_sites if keep_parity == 0 else self.geom.even_sites
+        if clover_is_zero(clover):
+            if self.diag == 0.0 or not np.isfinite(self.diag):
+                raise SingularBlockError(int(elim[0]), 0, float("inf"))
         require_device()
+        if not clover_is_zero(clover):
+            # eliminated diagonal blocks (4+m0) I - C: condition check as the
+            # reference (np.linalg.cond, oddeven.py:123-132), inverse packed like
+            # the clover (Hermitian) and uploaded once; applied in-kernel
+            keep = self.geom.even_sites if keep_parity == 0 else self.geom.odd_sites
+            blocks = self.diag * np.eye(6) - clover.blocks()[elim]
+            cond = np.linalg.cond(blocks)
+            bad = ~np.isfinite(cond) | (cond > cond_limit)
+            if bad.any():
+                row, half = np.argwhere(bad)[0]
+                raise SingularBlockError(int(elim[row]), int(half), float(cond[row, half]))
+            inv = np.linalg.inv(blocks)
+            rows, cols = np.tril_indices(6)
+            self.clover_inv = upload_packed_blocks(inv[..., rows, cols], dtype)
+            self.clover_keep = upload_packed_blocks(np.asarray(clover.data)[keep], dtype)
         self.gauge = gauge_dev if gauge_dev is not None else gauge_cache.get(gauge, dtype)
         self.lat = lattice if lattice is not None else _lattice(self.geom)
         self.comm = comm
@@ -131,11 +150,14 @@ class SchurOperator:
         return self.geom.n_sites // 2
 
     # -- device kernels ----------------------------------------------------------
-    def _hop(self, dst_parity, src, out, xself, alpha, beta, scale=None):
+    def _hop(self, dst_parity, src, out, xself, alpha, beta, scale=None, clover=None, mode=0):
         if self.comm is not None:
+            if clover is not None:
+                raise NotImplementedError("the T split implements C = 0")
             self.comm.hop(dst_parity, src, out, xself, alpha, beta, scale)
         else:
-            hop_device(self.lat, self.dtype, src.b, dst_parity, self.gauge, src, out, xself, alpha, beta, scale)
+            hop_device(self.lat, self.dtype, src.b, dst_parity, self.gauge, src, out, xself, alpha, beta, scale,
+                       clover=clover, clover_mode=mode)
 
     def _tmp_like(self, v: DeviceField) -> DeviceField:
         t = self._tmp
@@ -154,17 +176,28 @@ class SchurOperator:
         out = DeviceField.empty(v.n_sites, v.b, v.s, v.dtype, self.geom, self.keep_parity, v.layout) \
             if out is None else out
         a = self.diag
-        # tmp_o = D_oo^-1 (-D_oe) v = H_oe v / a
-        self._hop(self.elim_parity, v, tmp, None, 0.0, 1.0 / a)
-        # out_e = a v - H_eo tmp
-        self._hop(self.keep_parity, tmp, out, v, a, -1.0, scale)
+        if self.clover_inv is None:
+            # tmp_o = D_oo^-1 (-D_oe) v = H_oe v / a
+            self._hop(self.elim_parity, v, tmp, None, 0.0, 1.0 / a)
+            # out_e = a v - H_eo tmp
+            self._hop(self.keep_parity, tmp, out, v, a, -1.0, scale)
+        else:
+            # tmp_o = D_oo^-1 H_oe v ; out_e = (a - C_e) v - H_eo tmp
+            self._hop(self.elim_parity, v, tmp, None, 0.0, 1.0, None, self.clover_inv, 2)
+            self._hop(self.keep_parity, tmp, out, v, a, -1.0, scale, self.clover_keep, 1)
         return out
 
     def reduce_rhs_device(self, eta_keep: DeviceField, eta_elim: DeviceField) -> DeviceField:
         """eta~ = eta_k - D_ke D_ee^-1 eta_e = eta_k + H_ke eta_e / a (oddeven.py:179-188)."""
         out = eta_keep.empty_like()
         out.parity = self.keep_parity
-        self._hop(self.keep_parity, eta_elim, out, eta_keep, 1.0, 1.0 / self.diag)
+        if self.clover_inv is None:
+            self._hop(self.keep_parity, eta_elim, out, eta_keep, 1.0, 1.0 / self.diag)
+        else:
+            z = eta_elim.empty_like()
+            _lib.call("b200wd_clover_apply", eta_elim.n_sites, dtype_code(self.dtype), eta_elim.b,
+                      self.clover_inv.ptr, eta_elim.ptr, z.ptr, stream_ptr())
+            self._hop(self.keep_parity, z, out, eta_keep, 1.0, 1.0)
         return out
 
     def reconstruct_device(self, x_keep: DeviceField, eta_elim: DeviceField) -> DeviceField:
@@ -172,7 +205,10 @@ class SchurOperator:
         out = eta_elim.empty_like()
         out.parity = self.elim_parity
         a = self.diag
-        self._hop(self.elim_parity, x_keep, out, eta_elim, 1.0 / a, 1.0 / a)
+        if self.clover_inv is None:
+            self._hop(self.elim_parity, x_keep, out, eta_elim, 1.0 / a, 1.0 / a)
+        else:
+            self._hop(self.elim_parity, x_keep, out, eta_elim, 1.0, 1.0, None, self.clover_inv, 2)
         return out
 
     # -- reference-facing API -------------------------------------------------------

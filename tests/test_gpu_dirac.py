@@ -208,3 +208,74 @@ def test_tsplit_halo_kernels_reproduce_single_gpu(nranks, parity):
     got = torch.cat(outs, dim=0)
     err = (got - ref.data).abs().max().item() / ref.data.abs().max().item()
     assert err < 1e-14
+
+
+# ---- clover term (reference fixtures use random clover) ----
+
+
+def test_dirac_clover_matches_reference_golden():
+    f = load_npz("dirac_4444_clover.npz")
+    dims = tuple(int(x) for x in f["dims"])
+    geom = P.LatticeGeometry(dims)
+    gauge = P.GaugeField(geom, f["links"])
+    clover = P.CloverField(geom, f["clover_packed"])
+    psi = host_field(f["psi"], 2, geom)
+    eta = P.apply_dirac(P.DiracParams(m0=float(f["m0"])), gauge, clover, psi).ksi()
+    assert rel(eta, f["eta"]) < 1e-12
+    # Layout 1 input, c64
+    eta1 = P.apply_dirac(P.DiracParams(m0=float(f["m0"])), gauge, clover, host_field(f["psi"], 1, geom)).ksi()
+    assert rel(eta1, f["eta"]) < 1e-12
+    ref64 = O.apply_dirac(dims, float(f["m0"]), O.round_c64(f["links"]),
+                          O.round_c64(O.unpack_clover(f["clover_packed"])), O.round_c64(f["psi"]))
+    eta64 = P.apply_dirac(P.DiracParams(m0=float(f["m0"])), gauge, clover, psi, dtype="c64").ksi()
+    assert rel(eta64, ref64) < 1e-5
+
+
+def test_schur_clover_matches_reference_golden():
+    f = load_npz("schur_4444_clover.npz")
+    dims = (4, 4, 4, 4)
+    geom = P.LatticeGeometry(dims)
+    gauge = P.GaugeField(geom, O.gen_gauge_random(dims, 61))
+    clover = P.gen_clover(geom, "random", scale=0.1, seed=62)
+    s = P.SchurOperator(P.DiracParams(m0=-0.5), gauge, clover)
+    v = host_field(f["v"], 2)
+    assert rel(s.apply(v).ksi(), f["out"]) < 1e-12
+    eta = host_field(O.gen_spinor(256, 2, 73), 2, geom)
+    red, el = s.reduce_rhs(eta)
+    assert rel(red.ksi(), f["reduced"]) < 1e-12
+    assert rel(s.reconstruct(red, el).ksi(), f["x_odd"]) < 1e-12
+
+
+def test_schur_clover_keep_odd_matches_oracle():
+    dims = (4, 4, 4, 8)
+    geom = P.LatticeGeometry(dims)
+    links = O.gen_gauge_random(dims, 5)
+    cl = O.gen_clover_random(dims, 0.1, 6)
+    so = O.SchurOracle(dims, 0.2, links, cl, keep_parity=1)
+    v = O.gen_spinor(256, 3, 7)
+    sp = P.SchurOperator(P.DiracParams(m0=0.2), P.GaugeField(geom, links),
+                         P.CloverField(geom, O.pack_clover(cl)), keep_parity=1)
+    assert rel(sp.apply(host_field(v, 2)).ksi(), so.apply(v)) < 1e-12
+
+
+def test_gmres_clover_matches_reference_golden():
+    from tests.golden_util import load_gmres
+    g = load_gmres()["clover_4444_m1"]
+    dims = tuple(g["dims"])
+    geom = P.LatticeGeometry(dims)
+    gauge = P.GaugeField(geom, O.gen_gauge_random(dims, g["gauge_seed"]))
+    clover = P.gen_clover(geom, "random", scale=0.1, seed=g["clover_seed"])
+    eta = P.gen_spinor(256, g["b"], P.Layout.RHS_MAJOR, seed=g["eta_seed"], geom=geom)
+    res = P.gmres_solve(P.dirac_op(P.DiracParams(m0=g["m0"]), gauge, clover), eta, None,
+                        P.GmresConfig(tol=g["tol"], restarts=g["restarts"]))
+    assert abs(res.iterations - g["iterations"]) <= 1 and res.converged.all()
+    ref_h = np.array(g["history"])
+    k = min(len(ref_h), len(res.history))
+    live = ref_h[:k] > 1e-10
+    assert np.all(np.abs(np.array(res.history[:k]) - ref_h[:k])[live] <= 1e-8 * ref_h[:k][live])
+    # odd-even solve with clover agrees with the direct one
+    cfg = P.GmresConfig(tol=1e-10, restarts=40)
+    d = P.solve_dirac(P.DiracParams(m0=g["m0"]), gauge, clover, eta, cfg, odd_even=False)
+    s = P.solve_dirac(P.DiracParams(m0=g["m0"]), gauge, clover, eta, cfg, odd_even=True)
+    assert np.all(s.full_relnorms <= 1e-9) and s.iterations < d.iterations
+    assert np.abs(d.psi.ksi() - s.psi.ksi()).max() / np.abs(d.psi.ksi()).max() < 1e-7

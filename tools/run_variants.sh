@@ -1,3 +1,2 @@
 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-tail -2 gpurun_out/pytest_gpu.log
-python tools/sweep_dirac.py --iters 50 --bs 4 8 16
+tail -15 gpurun_out/pytest_gpu.log
