@@ -14,7 +14,8 @@ is one D_W apply of one nrhs block; steps rotate through enough distinct
 exceed 4x the L2 size (no L2 reuse across steps).  Batched GMRES
 time-to-solution on BASELINE configs[3] (24^3 x 48, nrhs=12, near-unit
 links, antiperiodic T, GMRES(30), tol 1e-10, full and odd-even) is added
-under "gmres" unless --no-gmres.
+under "gmres" and the configs[2] Schur apply (32^3 x 64, nrhs=12, c128)
+under "schur", unless --no-gmres.
 """
 
 from __future__ import annotations
@@ -388,6 +389,9 @@ def main():
     }
     if not args.no_gmres:
         line["gmres"] = gpu_gmres(args, torch, P)
+        sys.path.insert(0, str(ROOT / "tools"))
+        from bench_schur import schur_bench
+        line["schur"] = schur_bench()  # BASELINE configs[2]: 32^3x64 Schur apply, nrhs=12, c128
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample()
     print(json.dumps(line))
