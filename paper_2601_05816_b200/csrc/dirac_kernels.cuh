@@ -25,9 +25,6 @@
 
 namespace b200wd {
 
-#ifndef B200WD_PAIR_HOPS
-#define B200WD_PAIR_HOPS 0  // 1: consume the two tiles of one direction together (measured slower)
-#endif
 #ifndef B200WD_RING_NOMATH
 #define B200WD_RING_NOMATH 0  // experiment: consumers skip the t/x/y arithmetic
 #endif
@@ -209,14 +206,16 @@ __global__ void __launch_bounds__(kHopThreads, HopMinBlocks<R>::value) hop_kerne
 // (~200-300 cycles per CTA, tools/mb_tma.cu), so copies are kept few and big.
 // When an item covers whole z lines (NB*8 == Z) the z hops never leave the
 // item; otherwise the z-edge sites are read with ordinary loads.
-template <typename R, int V, int B, int NB_> struct RingShape {
+template <typename R, int V, int B, int NB_, bool PAR = false> struct RingShape {
+  static constexpr int F = PAR ? 2 : 1;                  // natural sites per field site
   static constexpr int BT = B / V;                       // threads per site
-  static constexpr int NB = NB_;                         // site blocks per item
+  static constexpr int NB = NB_;                         // field site blocks per item
   static constexpr int NC = BT * 8 * NB;                 // consumer threads
   static constexpr int NCW = NC / 32;                    // consumer warps
   static constexpr int NT = NC + 32;                     // + producer warp
   static constexpr int SPIN = NB * 96 * B;               // complex per spinor tile
-  static constexpr int SLOT = SPIN + NB * 72;            // + one link direction per block
+  static constexpr int LPB = 72 * F;                     // link complex per field block (one direction)
+  static constexpr int SLOT = SPIN + NB * LPB;           // + one link direction per block
   static constexpr int SLOT_BYTES = SLOT * (int)sizeof(cx<R>);
   static constexpr bool valid = (NC % 32 == 0) && NC >= 64 && NC <= 256 && (size_t)SLOT_BYTES * 2 <= 220 * 1024;
   static size_t smem(int S) { return (size_t)SLOT_BYTES * S + 16 * S; }
@@ -227,8 +226,8 @@ template <typename R, int V, int B, int NB_> struct RingShape {
 struct BlkCoord {
   int t, x, y, z0;
 };
-__device__ __forceinline__ BlkCoord block_coord(int64_t g, const HopParams& p) {
-  uint32_t s0 = (uint32_t)(g * 8);
+__device__ __forceinline__ BlkCoord block_coord(int64_t s0_nat, const HopParams& p) {
+  uint32_t s0 = (uint32_t)s0_nat;
   BlkCoord c;
   c.z0 = (int)(s0 % (uint32_t)p.Z);
   s0 /= (uint32_t)p.Z;
@@ -238,8 +237,9 @@ __device__ __forceinline__ BlkCoord block_coord(int64_t g, const HopParams& p) {
   c.t = (int)(s0 / (uint32_t)p.X);
   return c;
 }
+template <int F = 1>
 __device__ __forceinline__ void block_step(BlkCoord& c, const HopParams& p) {
-  c.z0 += 8;
+  c.z0 += 8 * F;
   if (c.z0 == p.Z) {
     c.z0 = 0;
     if (++c.y == p.Y) {
@@ -251,9 +251,9 @@ __device__ __forceinline__ void block_step(BlkCoord& c, const HopParams& p) {
     }
   }
 }
+// natural base site of the neighbour block (natural base s0 of the own block)
 template <int MU, bool FWD>
-__device__ __forceinline__ int64_t block_neighbor(int64_t g, const BlkCoord& c, const HopParams& p) {
-  const int64_t s0 = g * 8;
+__device__ __forceinline__ int64_t block_neighbor(int64_t s0, const BlkCoord& c, const HopParams& p) {
   const int64_t sY = p.Z, sX = (int64_t)p.Y * p.Z, sT = p.per_t;
   int64_t ns;
   if constexpr (MU == 0) ns = FWD ? (c.t + 1 == p.T ? s0 - (int64_t)(p.T - 1) * sT : s0 + sT)
@@ -262,61 +262,66 @@ __device__ __forceinline__ int64_t block_neighbor(int64_t g, const BlkCoord& c, 
                                        : (c.x == 0 ? s0 + (int64_t)(p.X - 1) * sX : s0 - sX);
   else ns = FWD ? (c.y + 1 == p.Y ? s0 - (int64_t)(p.Y - 1) * sY : s0 + sY)
                 : (c.y == 0 ? s0 + (int64_t)(p.Y - 1) * sY : s0 - sY);
-  return ns >> 3;
+  return ns;
 }
 __device__ __forceinline__ int64_t z_neighbor(int64_t d, int z, int Z, int step) {
   if (step > 0) return (z + 1 == Z) ? d - (Z - 1) : d + 1;
   return (z == 0) ? d + (Z - 1) : d - 1;
 }
 
-// tile H in 0..5: hop (mu = H/2, forward if H even); H == 6: own blocks (z tile)
-template <typename R, int V, int B, int NB, int H>
+// tile H in 0..5: hop (mu = H/2, forward if H even); H == 6: own blocks (z tile).
+// PAR: checkerboard fields (a field block of 8 cb sites = 16 natural sites of
+// one z line, Z % 16 == 0); links are always natural-site blocks.
+template <typename R, int V, int B, int NB, bool PAR, int H>
 __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, const BlkCoord& c0, cx<R>* slot,
                                            uint64_t* full) {
   using C = cx<R>;
-  using Sh = RingShape<R, V, B, NB>;
+  using Sh = RingShape<R, V, B, NB, PAR>;
+  constexpr int F = Sh::F;
   const C* src = static_cast<const C*>(p.src);
   const C* U = static_cast<const C*>(p.U);
-  const int64_t nblk = p.n >> 3;
+  const int64_t nblk = p.n >> 3;  // natural link blocks
   mbar_expect_tx(full, (uint32_t)(Sh::SLOT * sizeof(C)));
   if constexpr (H == 6) {
     bulk_g2s(slot, src + gb0 * 96 * B, Sh::SPIN * sizeof(C), full);
-    bulk_g2s(slot + Sh::SPIN, U + (3 * nblk + gb0) * 72, NB * 72 * sizeof(C), full);
+    bulk_g2s(slot + Sh::SPIN, U + (3 * nblk + F * gb0) * 72, NB * Sh::LPB * sizeof(C), full);
   } else {
     constexpr int MU = H >> 1;
     constexpr bool FWD = !(H & 1);
-    // neighbour blocks of the NB own blocks: contiguous unless a wrap falls inside the item
-    const int64_t nb0 = block_neighbor<MU, FWD>(gb0, c0, p);
+    // neighbour field blocks of the NB own blocks: contiguous unless a wrap falls inside the item
+    const int64_t nb0 = block_neighbor<MU, FWD>(gb0 * 8 * F, c0, p) / (8 * F);
     bool contiguous = true;
     if constexpr (NB > 1) {
       BlkCoord c = c0;
 #pragma unroll
       for (int jj = 1; jj < NB; ++jj) {
-        block_step(c, p);
-        contiguous &= block_neighbor<MU, FWD>(gb0 + jj, c, p) == nb0 + jj;
+        block_step<F>(c, p);
+        contiguous &= block_neighbor<MU, FWD>((gb0 + jj) * 8 * F, c, p) / (8 * F) == nb0 + jj;
       }
     }
     if (contiguous) {
       bulk_g2s(slot, src + nb0 * 96 * B, Sh::SPIN * sizeof(C), full);
-      bulk_g2s(slot + Sh::SPIN, U + (MU * nblk + (FWD ? gb0 : nb0)) * 72, NB * 72 * sizeof(C), full);
+      bulk_g2s(slot + Sh::SPIN, U + (MU * nblk + F * (FWD ? gb0 : nb0)) * 72, NB * Sh::LPB * sizeof(C), full);
     } else {
       BlkCoord c = c0;
 #pragma unroll
       for (int jj = 0; jj < NB; ++jj) {
-        if (jj) block_step(c, p);
-        const int64_t nb = block_neighbor<MU, FWD>(gb0 + jj, c, p);
+        if (jj) block_step<F>(c, p);
+        const int64_t nb = block_neighbor<MU, FWD>((gb0 + jj) * 8 * F, c, p) / (8 * F);
         bulk_g2s(slot + jj * 96 * B, src + nb * 96 * B, 96 * B * sizeof(C), full);
-        bulk_g2s(slot + Sh::SPIN + jj * 72, U + (MU * nblk + (FWD ? gb0 + jj : nb)) * 72, 72 * sizeof(C), full);
+        bulk_g2s(slot + Sh::SPIN + jj * Sh::LPB, U + (MU * nblk + F * (FWD ? gb0 + jj : nb)) * 72,
+                 Sh::LPB * sizeof(C), full);
       }
     }
   }
 }
 
-template <typename R, int V, int B, int NB>
-__global__ void __launch_bounds__(RingShape<R, V, B, NB>::NT) hop_ring_kernel(const HopParams p, int64_t n_items,
-                                                                              int S) {
+template <typename R, int V, int B, int NB, bool PAR>
+__global__ void __launch_bounds__(RingShape<R, V, B, NB, PAR>::NT) hop_ring_kernel(const HopParams p,
+                                                                                   int64_t n_items, int S) {
   using C = cx<R>;
-  using Sh = RingShape<R, V, B, NB>;
+  using Sh = RingShape<R, V, B, NB, PAR>;
+  constexpr int F = Sh::F;
   constexpr int KST = 8 * B;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   C* ring = reinterpret_cast<C*>(smem_raw);
@@ -339,16 +344,16 @@ __global__ void __launch_bounds__(RingShape<R, V, B, NB>::NT) hop_ring_kernel(co
       uint32_t pphase = 0;  // phase of the next fill of pslot; its release is phase^1 of empty
       for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int64_t gb0 = (p.d_begin >> 3) + it * NB;
-        const BlkCoord c0 = block_coord(gb0, p);
-#define B200WD_PRODUCE(H)                                                    \
-  {                                                                          \
-    if (pfirst == 0) mbar_wait(&empty[pslot], pphase ^ 1u);                  \
-    ring_issue<R, V, B, NB, H>(p, gb0, c0, ring + pslot * Sh::SLOT, &full[pslot]); \
-    if (++pslot == S) {                                                      \
-      pslot = 0;                                                             \
-      pphase ^= 1u;                                                          \
-      pfirst = 0;                                                            \
-    }                                                                        \
+        const BlkCoord c0 = block_coord(gb0 * 8 * F, p);
+#define B200WD_PRODUCE(H)                                                                   \
+  {                                                                                         \
+    if (pfirst == 0) mbar_wait(&empty[pslot], pphase ^ 1u);                                 \
+    ring_issue<R, V, B, NB, PAR, H>(p, gb0, c0, ring + pslot * Sh::SLOT, &full[pslot]);   \
+    if (++pslot == S) {                                                                     \
+      pslot = 0;                                                                            \
+      pphase ^= 1u;                                                                         \
+      pfirst = 0;                                                                           \
+    }                                                                                       \
   }
         B200WD_PRODUCE(6)
         B200WD_PRODUCE(0)
@@ -383,7 +388,16 @@ __global__ void __launch_bounds__(RingShape<R, V, B, NB>::NT) hop_ring_kernel(co
   uint32_t cphase = 0;
   for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
     const int64_t gb0 = (p.d_begin >> 3) + it * NB;
-    const int64_t d = (gb0 + j) * 8 + lo;
+    const int64_t d = (gb0 + j) * 8 + lo;  // field index of this thread's site
+    // natural site: full lattice d; checkerboard 2d + (parity fix of the block's line)
+    int64_t xn = d;
+    if constexpr (PAR) {
+      const BlkCoord cb = block_coord((gb0 + j) * 16, p);
+      xn = 2 * d + ((cb.t + cb.x + cb.y + p.par0 + p.dst_parity) & 1);
+    }
+    const int64_t nat0 = gb0 * 8 * F;        // natural base site of the item
+    const int li = (int)(xn - nat0);         // natural index inside the item's link blocks
+    const int lofs = (li >> 3) * 72 + (li & 7);
     C acc[V][12];
     {  // own blocks: xself, z hops
       const int slot = cslot;
@@ -406,25 +420,29 @@ __global__ void __launch_bounds__(RingShape<R, V, B, NB>::NT) hop_ring_kernel(co
 #pragma unroll
           for (int k = 0; k < 12; ++k) acc[v][k] = mk(R(0), R(0));
       }
-      const int z = (int)((uint32_t)d % (uint32_t)Z);
+      const int z = (int)((uint32_t)xn % (uint32_t)Z);
       {
-        const int64_t nd = z_neighbor(d, z, Z, 1);
-        const int64_t jb = (nd >> 3) - gb0;
-        const C* ul = zt + Sh::SPIN + j * 72 + lo;  // U_3(x), own blocks
+        const int64_t xp = z_neighbor(xn, z, Z, 1);
+        const int64_t fi = PAR ? (xp >> 1) : xp;
+        const int64_t jb = (fi >> 3) - gb0;
+        const C* ul = zt + Sh::SPIN + lofs;  // U_3(x), own blocks
         if (jb >= 0 && jb < NB)
-          hop_full<3, true, R, V, true, true>(acc, zt + jb * 96 * B + (nd & 7) * B + r0, KST, ul, 8);
+          hop_full<3, true, R, V, true, true>(acc, zt + jb * 96 * B + (fi & 7) * B + r0, KST, ul, 8);
         else
-          hop_full<3, true, R, V, false, true>(acc, src + spinor_base(nd, 12, B) + r0, KST, ul, 8);
+          hop_full<3, true, R, V, false, true>(acc, src + spinor_base(fi, 12, B) + r0, KST, ul, 8);
       }
       {
-        const int64_t nd = z_neighbor(d, z, Z, -1);
-        const int64_t jb = (nd >> 3) - gb0;
-        if (jb >= 0 && jb < NB)
-          hop_full<3, false, R, V, true, true>(acc, zt + jb * 96 * B + (nd & 7) * B + r0, KST,
-                                               zt + Sh::SPIN + jb * 72 + (nd & 7), 8);
+        const int64_t xp = z_neighbor(xn, z, Z, -1);
+        const int64_t fi = PAR ? (xp >> 1) : xp;
+        const int64_t jb = (fi >> 3) - gb0;
+        const int lj = (int)(xp - nat0);
+        const bool lin = lj >= 0 && lj < 8 * F * NB;
+        if (jb >= 0 && jb < NB && lin)
+          hop_full<3, false, R, V, true, true>(acc, zt + jb * 96 * B + (fi & 7) * B + r0, KST,
+                                               zt + Sh::SPIN + (lj >> 3) * 72 + (lj & 7), 8);
         else
-          hop_full<3, false, R, V, false, false>(acc, src + spinor_base(nd, 12, B) + r0, KST,
-                                                 U + link_base(nd, 3, nblk), 8);
+          hop_full<3, false, R, V, false, false>(acc, src + spinor_base(fi, 12, B) + r0, KST,
+                                                 U + link_base(xp, 3, nblk), 8);
       }
       __syncwarp();
       if (lead) mbar_arrive(&empty[slot]);
@@ -434,42 +452,6 @@ __global__ void __launch_bounds__(RingShape<R, V, B, NB>::NT) hop_ring_kernel(co
       }
     }
 
-#if B200WD_PAIR_HOPS
-    // forward + backward tile of one direction together: two independent hops
-    // in one basic block give the scheduler twice the ILP
-#define B200WD_CONSUME_PAIR(H)                                                                        \
-  {                                                                                                  \
-    const int sa = cslot;                                                                            \
-    const uint32_t pa = cphase;                                                                      \
-    if (++cslot == S) {                                                                              \
-      cslot = 0;                                                                                     \
-      cphase ^= 1u;                                                                                  \
-    }                                                                                                \
-    const int sb_ = cslot;                                                                           \
-    const uint32_t pb = cphase;                                                                      \
-    if (++cslot == S) {                                                                              \
-      cslot = 0;                                                                                     \
-      cphase ^= 1u;                                                                                  \
-    }                                                                                                \
-    mbar_wait(&full[sa], pa);                                                                        \
-    mbar_wait(&full[sb_], pb);                                                                       \
-    const C* ta = ring + sa * Sh::SLOT;                                                              \
-    const C* tb = ring + sb_ * Sh::SLOT;                                                             \
-    hop_full<((H) >> 1), true, R, V, true, true>(acc, ta + j * 96 * B + lo * B + r0, KST,            \
-                                                 ta + Sh::SPIN + j * 72 + lo, 8);                    \
-    hop_full<((H) >> 1), false, R, V, true, true>(acc, tb + j * 96 * B + lo * B + r0, KST,           \
-                                                  tb + Sh::SPIN + j * 72 + lo, 8);                   \
-    __syncwarp();                                                                                    \
-    if (lead) {                                                                                      \
-      mbar_arrive(&empty[sa]);                                                                       \
-      mbar_arrive(&empty[sb_]);                                                                      \
-    }                                                                                                \
-  }
-    B200WD_CONSUME_PAIR(0)
-    B200WD_CONSUME_PAIR(2)
-    B200WD_CONSUME_PAIR(4)
-#undef B200WD_CONSUME_PAIR
-#else
 #define B200WD_CONSUME(H)                                                                            \
   {                                                                                                  \
     const int slot = cslot;                                                                          \
@@ -477,7 +459,7 @@ __global__ void __launch_bounds__(RingShape<R, V, B, NB>::NT) hop_ring_kernel(co
     const C* sb = ring + slot * Sh::SLOT;                                                            \
     if (!B200WD_RING_NOMATH)                                                                         \
       hop_full<((H) >> 1), !((H)&1), R, V, true, true>(acc, sb + j * 96 * B + lo * B + r0, KST,      \
-                                                        sb + Sh::SPIN + j * 72 + lo, 8);             \
+                                                        sb + Sh::SPIN + lofs, 8);                    \
     __syncwarp();                                                                                    \
     if (lead) mbar_arrive(&empty[slot]);                                                             \
     if (++cslot == S) {                                                                              \
@@ -492,7 +474,6 @@ __global__ void __launch_bounds__(RingShape<R, V, B, NB>::NT) hop_ring_kernel(co
     B200WD_CONSUME(4)
     B200WD_CONSUME(5)
 #undef B200WD_CONSUME
-#endif
 
     C* out = static_cast<C*>(p.out) + spinor_base(d, 12, B) + r0;
 #pragma unroll
@@ -524,9 +505,9 @@ static RingCfg ring_env() {
   return c;
 }
 
-template <typename R, int V, int B, int NB>
+template <typename R, int V, int B, int NB, bool PAR>
 static bool launch_ring_nb(const HopParams& p, int64_t nblk, int S, cudaStream_t st) {
-  using Sh = RingShape<R, V, B, NB>;
+  using Sh = RingShape<R, V, B, NB, PAR>;
   if constexpr (!Sh::valid) {
     return false;
   } else {
@@ -534,17 +515,18 @@ static bool launch_ring_nb(const HopParams& p, int64_t nblk, int S, cudaStream_t
     if (S <= 0) S = (Sh::SLOT_BYTES >= 40 * 1024) ? (200 * 1024) / Sh::SLOT_BYTES : (100 * 1024) / Sh::SLOT_BYTES;
     if (S < 2) S = 2;
     if (S > 8) S = 8;
-    const size_t smem = Sh::smem(S);
+    size_t smem = Sh::smem(S);
+    while (smem > 227 * 1024 && S > 2) smem = Sh::smem(--S);
     static size_t attr_smem = 0;
     if (attr_smem < smem) {
-      if (cudaFuncSetAttribute(hop_ring_kernel<R, V, B, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      if (cudaFuncSetAttribute(hop_ring_kernel<R, V, B, NB, PAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem) != cudaSuccess)
         return false;
       attr_smem = smem;
     }
     int ctas_per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, hop_ring_kernel<R, V, B, NB>, Sh::NT, smem) !=
-            cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, hop_ring_kernel<R, V, B, NB, PAR>, Sh::NT,
+                                                      smem) != cudaSuccess ||
         ctas_per_sm <= 0)
       return false;
     static int sm_count = 0;
@@ -556,7 +538,7 @@ static bool launch_ring_nb(const HopParams& p, int64_t nblk, int S, cudaStream_t
     const int64_t n_items = nblk / NB;
     int64_t grid = (int64_t)ctas_per_sm * sm_count;
     if (grid > n_items) grid = n_items;
-    hop_ring_kernel<R, V, B, NB><<<(unsigned)grid, Sh::NT, smem, st>>>(p, n_items, S);
+    hop_ring_kernel<R, V, B, NB, PAR><<<(unsigned)grid, Sh::NT, smem, st>>>(p, n_items, S);
     return true;
   }
 }
@@ -593,33 +575,66 @@ static RingCfg ring_table(int Z) {
 
 // Launch the ring kernel when its shape preconditions hold (full lattice, no
 // halos, Z % 8 == 0); false -> the caller uses the generic kernel.
+static bool par_ring_enabled() {
+  static int en = -1;
+  if (en < 0) {
+    const char* e = getenv("B200WD_PAR_RING");
+    en = (e && e[0] == '0') ? 0 : 1;
+  }
+  return en == 1;
+}
+
+template <typename R, int V, int B, bool PAR>
+static bool try_launch_ring_par(const HopParams& p, int64_t nblk, RingCfg c, cudaStream_t st) {
+  constexpr int F = PAR ? 2 : 1;
+  const int line = p.Z / (8 * F);  // field blocks per z line
+  if (c.nb <= 0) c.nb = line;
+  switch (c.nb) {
+    case 4:
+      if (launch_ring_nb<R, V, B, 4, PAR>(p, nblk, c.s, st)) return true;
+      break;
+    case 2:
+      if (launch_ring_nb<R, V, B, 2, PAR>(p, nblk, c.s, st)) return true;
+      break;
+    case 1:
+      if (launch_ring_nb<R, V, B, 1, PAR>(p, nblk, c.s, st)) return true;
+      break;
+    default:
+      break;
+  }
+  // partial lines: the z edges use ordinary loads
+  if (launch_ring_nb<R, V, B, 2, PAR>(p, nblk, 0, st)) return true;
+  return launch_ring_nb<R, V, B, 1, PAR>(p, nblk, 0, st);
+}
+
+// Launch the ring kernel when its shape preconditions hold (no halos, no
+// clover; full lattice: Z % 8 == 0; checkerboard fields: Z % 16 == 0); false
+// -> the caller uses the generic kernel.
 template <typename R, int V, int B>
 static bool try_launch_ring(const HopParams& p, cudaStream_t st) {
-  if (p.dst_parity >= 0 || p.lam_halo != nullptr || p.Z % 8 != 0 || p.beta == 0.0 || p.clov_mode != 0)
-    return false;
+  if (p.lam_halo != nullptr || p.beta == 0.0 || p.clov_mode != 0) return false;
+  const bool par = p.dst_parity >= 0;
+  if (p.Z % (par ? 16 : 8) != 0) return false;
   if ((p.d_begin & 7) || (p.d_end & 7)) return false;
   const int64_t nblk = (p.d_end - p.d_begin) >> 3;
   const RingCfg env = ring_env();
   RingCfg c = ring_table<R, V, B>(p.Z);
   if (env.nb > 0) c.nb = env.nb;
   if (env.s > 0) c.s = env.s;
-  if (c.nb <= 0) c.nb = p.Z / 8;  // whole z lines per item
-  switch (c.nb) {
-    case 4:
-      if (launch_ring_nb<R, V, B, 4>(p, nblk, c.s, st)) return true;
-      break;
-    case 2:
-      if (launch_ring_nb<R, V, B, 2>(p, nblk, c.s, st)) return true;
-      break;
-    case 1:
-      if (launch_ring_nb<R, V, B, 1>(p, nblk, c.s, st)) return true;
-      break;
-    default:
-      break;
+  if (par) {
+    if (!par_ring_enabled()) return false;
+    // measured (tools/sweep_dirac.py --parity 0 on 32^3x64): (NB, S) per nrhs
+    RingCfg cp{};
+    if constexpr (sizeof(R) == 8) {
+      if (B == 4 || B == 8) cp = RingCfg{2, 3};
+    } else {
+      if (B == 8) cp = RingCfg{2, 3};
+    }
+    if (env.nb > 0) cp.nb = env.nb;
+    if (env.s > 0) cp.s = env.s;
+    return try_launch_ring_par<R, V, B, true>(p, nblk, cp, st);
   }
-  // partial lines: the z edges use ordinary loads
-  if (launch_ring_nb<R, V, B, 2>(p, nblk, 0, st)) return true;
-  return launch_ring_nb<R, V, B, 1>(p, nblk, 0, st);
+  return try_launch_ring_par<R, V, B, false>(p, nblk, c, st);
 }
 
 // ---- site-local block apply: out = M x (D_oo^-1 eta_o of reduce_rhs) ---------

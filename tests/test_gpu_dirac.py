@@ -279,3 +279,43 @@ def test_gmres_clover_matches_reference_golden():
     s = P.solve_dirac(P.DiracParams(m0=g["m0"]), gauge, clover, eta, cfg, odd_even=True)
     assert np.all(s.full_relnorms <= 1e-9) and s.iterations < d.iterations
     assert np.abs(d.psi.ksi() - s.psi.ksi()).max() / np.abs(d.psi.ksi()).max() < 1e-7
+
+
+@pytest.mark.parametrize("dims", [(4, 4, 4, 16), (4, 2, 2, 32), (6, 2, 4, 16)])
+@pytest.mark.parametrize("b,dtype,tol", [(4, "c128", 1e-12), (12, "c128", 1e-12), (8, "c64", 1e-5),
+                                         (16, "c64", 1e-5)])
+def test_schur_ring_path_matches_oracle(dims, b, dtype, tol):
+    """Z % 16 == 0 lattices take the checkerboard TMA ring kernel."""
+    geom = P.LatticeGeometry(dims)
+    links = O.flip_time_boundary(O.near_unit_gauge(dims, 0.3, 17), dims)
+    v = O.gen_spinor(geom.n_sites // 2, b, 18)
+    for keep in (0, 1):
+        so = O.SchurOracle(dims, 0.1, O.round_c64(links) if dtype == "c64" else links, None, keep_parity=keep)
+        ref = so.apply(O.round_c64(v) if dtype == "c64" else v)
+        sp = P.SchurOperator(P.DiracParams(m0=0.1), P.GaugeField(geom, links), None, keep_parity=keep, dtype=dtype)
+        from paper_2601_05816_b200.device import upload
+        got = sp.apply_device(upload(host_field(v, 2), dtype, parity=keep)).logical()
+        assert rel(got, ref) < tol
+    # reduce_rhs / reconstruct on the same lattice
+    eta = O.gen_spinor(geom.n_sites, b, 19)
+    so = O.SchurOracle(dims, 0.1, links, None)
+    red_ref, el_ref = so.reduce_rhs(eta)
+    sp = P.SchurOperator(P.DiracParams(m0=0.1), P.GaugeField(geom, links), None)
+    red, el = sp.reduce_rhs(host_field(eta, 2, geom))
+    assert rel(red.ksi(), red_ref) < 1e-12
+    assert rel(sp.reconstruct(red, el).ksi(), so.reconstruct(red_ref, el_ref)) < 1e-12
+
+
+@pytest.mark.parametrize("dims", [(4, 4, 4, 16), (4, 2, 6, 24), (4, 2, 2, 32)])
+@pytest.mark.parametrize("b", [4, 6, 12, 16, 24, 32])
+def test_ring_full_lattice_shapes(dims, b):
+    """Z = 16, 24, 32 exercise whole-line and partial-line (z-edge) ring items."""
+    geom = P.LatticeGeometry(dims)
+    links = O.near_unit_gauge(dims, 0.3, 23)
+    psi = O.gen_spinor(geom.n_sites, b, 24)
+    ref = O.apply_dirac(dims, 0.1, links, None, psi)
+    got = P.apply_dirac(P.DiracParams(m0=0.1), P.GaugeField(geom, links), None, host_field(psi, 2, geom))
+    assert rel(got.ksi(), ref) < 1e-12
+    got64 = P.apply_dirac(P.DiracParams(m0=0.1), P.GaugeField(geom, links), None, host_field(psi, 2, geom),
+                          dtype="c64")
+    assert rel(got64.ksi(), O.apply_dirac(dims, 0.1, O.round_c64(links), None, O.round_c64(psi))) < 1e-5

@@ -1,2 +1,2 @@
 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-tail -15 gpurun_out/pytest_gpu.log
+tail -3 gpurun_out/pytest_gpu.log
