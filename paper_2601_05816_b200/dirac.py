@@ -146,6 +146,73 @@ class DiracOperator:
                    clover=self.clover, clover_mode=1, stream=stream)
         return out
 
+    def apply_range(self, v: DeviceField, out: DeviceField, t_begin: int, t_end: int, stream=None) -> None:
+        """Write only the T slices [t_begin, t_end) of out = D v."""
+        hop_device(self.lat, self.dtype, v.b, -1, self.gauge, v, out, v, 4.0 + self.params.m0, -1.0, None,
+                   t_begin, t_end, clover=self.clover, clover_mode=1, stream=stream)
+
+    def apply_host_pipelined(self, psi, out=None, chunks: int = 8):
+        """Host field in -> host field out with the PCIe transfers overlapped.
+
+        The lattice is cut into T-slab chunks.  Chunk c is copied H2D and
+        converted to the device layout on an upload stream; as soon as chunk
+        c+1 has landed, the D slices of chunk c are computed (their t+1
+        neighbours are now resident), converted back and copied D2H on a
+        download stream, so uploads, compute and downloads of different chunks
+        overlap (PCIe is full duplex).  Chunk 0 waits for the last chunk (the
+        periodic T wrap).  Results are identical to the unpipelined apply.
+        """
+        import torch
+
+        T = self.geom.dims[0]
+        nck = max(d for d in range(1, min(chunks, T) + 1) if T % d == 0)
+        if nck < 2:
+            return self.apply_device(upload(psi, self.dtype)).to_host(psi.layout, out)
+        tc = T // nck
+        per_t = self.geom.sites_per_slice
+        n, b, s = psi.n_sites, psi.b, psi.s
+        layout = int(psi.layout)
+        if out is None:
+            from .fields import BlockSpinorField
+            out = BlockSpinorField.zeros(n, b, layout, s, self.geom)
+        host_in = torch.from_numpy(np.ascontiguousarray(np.asarray(psi.data)).reshape(-1))
+        host_out = torch.from_numpy(out.data.reshape(-1))
+        dev = require_device()
+        raw_in = torch.empty(n * s * b, dtype=torch.complex128, device=dev)
+        raw_out = torch.empty_like(raw_in)
+        d_psi = DeviceField.empty(n, b, s, self.dtype, self.geom)
+        d_eta = DeviceField.empty(n, b, s, self.dtype, self.geom)
+        cur = torch.cuda.current_stream()
+        s_up, s_dn = torch.cuda.Stream(), torch.cuda.Stream()
+        s_up.wait_stream(cur)
+        chunk = tc * per_t * s * b  # complex elements per chunk (both layouts are site-major)
+        esz = d_psi.data.element_size()
+        up_ev = []
+        with torch.cuda.stream(s_up):
+            for c in range(nck):
+                sl = slice(c * chunk, (c + 1) * chunk)
+                raw_in[sl].copy_(host_in[sl], non_blocking=True)
+                _lib.call("b200wd_spinor_import", raw_in[sl].data_ptr(), layout, tc * per_t, s, b,
+                          d_psi.ptr + c * chunk * esz, dtype_code(self.dtype), stream_ptr(s_up))
+                ev = torch.cuda.Event()
+                ev.record(s_up)
+                up_ev.append(ev)
+        order = list(range(1, nck)) + [0]
+        for c in order:
+            cur.wait_event(up_ev[(c + 1) % nck])
+            if c == 0:
+                cur.wait_event(up_ev[0])
+            self.apply_range(d_psi, d_eta, c * tc, (c + 1) * tc, cur)
+            sl = slice(c * chunk, (c + 1) * chunk)
+            _lib.call("b200wd_spinor_export", d_eta.ptr + c * chunk * esz, dtype_code(self.dtype), tc * per_t, s,
+                      b, raw_out[sl].data_ptr(), layout, stream_ptr(cur))
+            s_dn.wait_stream(cur)
+            with torch.cuda.stream(s_dn):
+                host_out[sl].copy_(raw_out[sl], non_blocking=True)
+        s_dn.synchronize()
+        cur.wait_stream(s_dn)
+        return out
+
     def __call__(self, v):
         return _apply_any(self, v)
 
@@ -179,7 +246,7 @@ def apply_dirac(params: DiracParams, gauge, clover, psi, comm=None, flops: FlopC
     if isinstance(psi, DeviceField):
         res = op.apply_device(psi, out)
     else:
-        res = op.apply_device(upload(psi, dtype)).to_host(psi.layout, out)
+        res = op.apply_host_pipelined(psi, out)
     if flops is not None:
         flops.add_apply(psi.n_sites, psi.b)
     if perf is not None:

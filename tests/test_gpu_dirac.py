@@ -319,3 +319,24 @@ def test_ring_full_lattice_shapes(dims, b):
     got64 = P.apply_dirac(P.DiracParams(m0=0.1), P.GaugeField(geom, links), None, host_field(psi, 2, geom),
                           dtype="c64")
     assert rel(got64.ksi(), O.apply_dirac(dims, 0.1, O.round_c64(links), None, O.round_c64(psi))) < 1e-5
+
+
+@pytest.mark.parametrize("layout", [1, 2])
+def test_host_pipelined_apply_matches_device_apply(layout):
+    """apply_dirac on host fields overlaps H2D/compute/D2H over T chunks."""
+    import torch
+    dims = (16, 4, 4, 8)
+    geom = P.LatticeGeometry(dims)
+    links = O.flip_time_boundary(O.near_unit_gauge(dims, 0.3, 31), dims)
+    psi = O.gen_spinor(geom.n_sites, 4, 32)
+    ref = O.apply_dirac(dims, 0.1, links, None, psi)
+    n = geom.n_sites
+    pin_in = torch.empty(n * 48, dtype=torch.complex128).pin_memory()
+    pin_out = torch.empty(n * 48, dtype=torch.complex128).pin_memory()
+    f = P.BlockSpinorField(n, 12, 4, P.Layout(layout), pin_in.numpy(), geom)
+    f.set_ksi(psi)
+    o = P.BlockSpinorField(n, 12, 4, P.Layout(layout), pin_out.numpy(), geom)
+    for chunks in (1, 2, 4, 8, 16):
+        op = P.DiracOperator(P.DiracParams(m0=0.1), P.GaugeField(geom, links), None)
+        op.apply_host_pipelined(f, o, chunks=chunks)
+        assert rel(o.ksi(), ref) < 1e-12
