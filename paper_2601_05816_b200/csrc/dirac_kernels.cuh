@@ -25,6 +25,9 @@
 
 namespace b200wd {
 
+#ifndef B200WD_L2_PREFETCH
+#define B200WD_L2_PREFETCH 0  // items ahead for L2 prefetch of compulsory misses (0: off)
+#endif
 #ifndef B200WD_RING_NOMATH
 #define B200WD_RING_NOMATH 0  // experiment: consumers skip the t/x/y arithmetic
 #endif
@@ -345,6 +348,23 @@ __global__ void __launch_bounds__(RingShape<R, V, B, NB, PAR>::NT) hop_ring_kern
       for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int64_t gb0 = (p.d_begin >> 3) + it * NB;
         const BlkCoord c0 = block_coord(gb0 * 8 * F, p);
+#if B200WD_L2_PREFETCH
+        {  // warm L2 with the compulsory misses of a later item of this CTA:
+           // its t+1 neighbour blocks (first touch in sweep order) and links
+          const int64_t nx = it + (int64_t)B200WD_L2_PREFETCH * gridDim.x;
+          if (nx < n_items) {
+            const int64_t gn = (p.d_begin >> 3) + nx * NB;
+            const BlkCoord cn = block_coord(gn * 8 * F, p);
+            const int64_t nb = block_neighbor<0, true>(gn * 8 * F, cn, p) / (8 * F);
+            const C* srcp = static_cast<const C*>(p.src);
+            const C* Up = static_cast<const C*>(p.U);
+            bulk_prefetch_l2(srcp + nb * 96 * B, Sh::SPIN * sizeof(C));
+            const int64_t nbl = p.n >> 3;
+#pragma unroll
+            for (int mu = 0; mu < 4; ++mu) bulk_prefetch_l2(Up + (mu * nbl + F * gn) * 72, NB * Sh::LPB * sizeof(C));
+          }
+        }
+#endif
 #define B200WD_PRODUCE(H)                                                                   \
   {                                                                                         \
     if (pfirst == 0) mbar_wait(&empty[pslot], pphase ^ 1u);                                 \
