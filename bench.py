@@ -338,7 +338,7 @@ def multi_gpu(args, torch, P):
                        "l2": "2 rotating buffers of 403 MB (> L2)"},
             "roofline": {"bound": "hbm", "achieved": alg / tt / 1e9, "peak": hbm_peak, "unit": "GB/s",
                          "frac": alg / tt / 1e9 / hbm_peak, "traffic": None, "peak_kind": peak_kind},
-            "gpu_launches": 4 * args.steps, "clocks": clk,
+            "gpu_launches": (4 if world > 1 else 1) * args.steps, "clocks": clk,
             "halo_bytes_per_step_per_rank": comm.stats["bytes_sent"] / max(1, comm.stats["applies"]),
         }
         print(json.dumps(line))
@@ -352,6 +352,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-gmres", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--force-dist", action="store_true", help="run the T-split path even with one rank")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -359,7 +360,7 @@ def main():
         return reference_arm(args)
     import torch
     import paper_2601_05816_b200 as P
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.force_dist:
         import torch.distributed as dist
         dist.init_process_group("nccl")
         try:

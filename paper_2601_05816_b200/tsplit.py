@@ -36,6 +36,10 @@ from .fields import SPINOR_LEN
 from .geometry import LatticeGeometry, t_split
 
 
+def _real_view(t: torch.Tensor) -> torch.Tensor:
+    return torch.view_as_real(t) if t.is_complex() else t
+
+
 class CudaHaloKernels:
     """Device kernels used by the T split (libb200wd)."""
 
@@ -81,7 +85,7 @@ class TSplitComm:
     def allreduce(self, t: torch.Tensor) -> torch.Tensor:
         """Sum per-rank partial reductions (GMRES dots / norms) in place."""
         if self.world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+            dist.all_reduce(_real_view(t), op=dist.ReduceOp.SUM, group=self.group)
         return t
 
     def _face_buffers(self, parity, b, dtype, device):
@@ -98,11 +102,12 @@ class TSplitComm:
             lam_in.copy_(lam)
             chi_in.copy_(chi)
             return []
+        # complex faces travel as their real views (NCCL has no complex dtype)
         ops = [
-            dist.P2POp(dist.isend, lam, self.down, self.group, tag=1),
-            dist.P2POp(dist.irecv, lam_in, self.up, self.group, tag=1),
-            dist.P2POp(dist.isend, chi, self.up, self.group, tag=2),
-            dist.P2POp(dist.irecv, chi_in, self.down, self.group, tag=2),
+            dist.P2POp(dist.isend, _real_view(lam), self.down, self.group, tag=1),
+            dist.P2POp(dist.irecv, _real_view(lam_in), self.up, self.group, tag=1),
+            dist.P2POp(dist.isend, _real_view(chi), self.up, self.group, tag=2),
+            dist.P2POp(dist.irecv, _real_view(chi_in), self.down, self.group, tag=2),
         ]
         self.stats["bytes_sent"] += 2 * lam.numel() * lam.element_size()
         return dist.batch_isend_irecv(ops)
