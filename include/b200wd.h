@@ -18,15 +18,19 @@
  *    returns a message (thread-local).  No C++ exception crosses the ABI.
  *  - dtype: B200WD_C128 (complex128, double2) or B200WD_C64 (complex64,
  *    float2).  Scalars are always passed as double.
- *  - Device spinor layout ("component planes"): element (k, site, r) of a
- *    field with s components, n sites and b right-hand sides lives at
- *    ((k*n + site)*b + r).  rhs is innermost, so a warp's loads of one
- *    component over consecutive (site, rhs) pairs are contiguous.  Parity
+ *  - Device spinor layout ("site-blocked component planes", n % 8 == 0):
+ *    element (site, k, r) of a field with s components and b right-hand
+ *    sides lives at (((site>>3)*s + k)*8 + (site&7))*b + r, i.e. blocks of 8
+ *    sites in which component k of the 8 sites is one contiguous run of 8*b
+ *    complex numbers.  rhs is innermost, so a warp's loads of one component
+ *    over consecutive (site, rhs) pairs are contiguous.  Parity
  *    (checkerboard) fields use n/2 sites indexed by cb = site >> 1, which
  *    equals the reference's ascending-natural-order parity numbering
  *    (oddeven.py:62-65) because the fastest extent is even.
- *  - Device link layout: element (mu, e=3*row+col, site) at
- *    ((mu*9 + e)*n + site).
+ *  - Device link layout, direction-major: element (site, mu, e=3*row+col)
+ *    at ((mu*(n/8) + (site>>3))*9 + e)*8 + (site&7).
+ *  - Clover blocks: 2 x 21 packed complex per site, element (site, q) at
+ *    ((site>>3)*42 + q)*8 + (site&7).
  *  - Lattice: extents (T,X,Y,Z) = dims[0..3], site = ((t*X+x)*Y+y)*Z+z,
  *    T slowest (geometry.py:1-11).  Time is direction 0.
  */
@@ -39,7 +43,7 @@
 extern "C" {
 #endif
 
-#define B200WD_ABI_VERSION 1
+#define B200WD_ABI_VERSION 2
 
 #define B200WD_OK 0
 #define B200WD_ERR_ARG 1         /* bad shape / layout / parameter -> ValueError      */
@@ -206,6 +210,60 @@ int b200wd_gmres_close_column(const b200wd_gmres_state* st, int32_t j, void* str
  * psi += sum_{p<j_done} y_p sigma_p Z_p in one pass (gmres.py:226-229). */
 int b200wd_gmres_update(const b200wd_gmres_state* st, int32_t j_done, int64_t n_sites,
                         int32_t s, const void* const* z, void* psi, void* stream);
+
+/* ---- operator programs and the native Arnoldi step ---------------------- */
+/* A linear operator as a short program of hop stages, so the library can
+ * apply it without a round trip through the host language (the reference's
+ * LinearOperator protocol, operator.py:1-40).  Each stage is one
+ * b200wd_hop_clover launch over all local slices; its src / xself / out are
+ * picked from the call's input (B200WD_OPND_IN), output (B200WD_OPND_OUT) or
+ * the program's scratch field `tmp` (B200WD_OPND_TMP).  The call's `scale`
+ * array goes to the stages with use_scale = 1.
+ *   full D_W (dirac.py:266-305):      1 stage, dst_parity -1,
+ *                                     src = xself = IN, out = OUT
+ *   Schur S = D_kk - D_ke D_ee^-1 D_ek (oddeven.py:165-174):
+ *                                     stage 0 dst = elim parity, IN -> TMP
+ *                                     stage 1 dst = keep parity, TMP -> OUT,
+ *                                             xself = IN                    */
+#define B200WD_OPND_NONE 0
+#define B200WD_OPND_IN 1
+#define B200WD_OPND_OUT 2
+#define B200WD_OPND_TMP 3
+#define B200WD_MAX_STAGES 4
+
+typedef struct b200wd_hop_stage {
+  int32_t dst_parity;   /* -1 full lattice, 0|1 checkerboard                   */
+  int32_t src, xself, out; /* B200WD_OPND_*                                    */
+  double alpha, beta;   /* as b200wd_hop_clover                                 */
+  const void* clover;   /* packed blocks or NULL                                */
+  int32_t clover_mode;  /* 0, 1, 2 as b200wd_hop_clover                         */
+  int32_t use_scale;    /* 1: multiply by the call's scale[b]                   */
+} b200wd_hop_stage;
+
+typedef struct b200wd_operator {
+  b200wd_lattice lat;
+  int32_t dtype;
+  int32_t n_stages;     /* 1 .. B200WD_MAX_STAGES                               */
+  const void* links;
+  void* tmp;            /* scratch field for B200WD_OPND_TMP (or NULL)          */
+  b200wd_hop_stage stage[B200WD_MAX_STAGES];
+} b200wd_operator;
+
+/* out = op(in) (scale: device array of b doubles or NULL). */
+int b200wd_operator_apply(const b200wd_operator* op, int32_t b, const void* in, void* out,
+                          const double* scale, void* stream);
+
+/* One whole Arnoldi step of column j on a single rank (gmres.py:108-157):
+ * Z_{j+1} = sigma_j op(Z_j), the fused MGS sweep against Z_0..Z_j, the column
+ * close (breakdown test, Givens rotation, relnorm), then the relnorm of every
+ * rhs is copied into relnorm_host (b doubles, pinned host memory) and the
+ * stream is synchronised, so the caller can run the reference's stop test.
+ * Equivalent to b200wd_operator_apply + b200wd_gmres_dot + (j+1) x
+ * b200wd_gmres_mgs + b200wd_gmres_close_column, issued from native code.
+ * relnorm_host may be NULL (no copy, no synchronisation). */
+int b200wd_gmres_arnoldi(const b200wd_gmres_state* st, const b200wd_operator* op, int32_t j,
+                         int64_t n_sites, const void* const* z, double* relnorm_host,
+                         void* stream);
 
 #ifdef __cplusplus
 }

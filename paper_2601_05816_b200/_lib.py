@@ -17,7 +17,7 @@ LIB_PATH = Path(os.environ.get("B200WD_LIB") or Path(__file__).resolve().parent 
 
 OK, ERR_ARG, ERR_CUDA, ERR_SINGULAR, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 C128, C64 = 0, 1
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class B200Unavailable(RuntimeError):
@@ -45,9 +45,51 @@ class GmresState(C.Structure):
     ]
 
 
+OPND_NONE, OPND_IN, OPND_OUT, OPND_TMP = 0, 1, 2, 3
+MAX_STAGES = 4
+
+
+class HopStage(C.Structure):
+    _fields_ = [
+        ("dst_parity", C.c_int32), ("src", C.c_int32), ("xself", C.c_int32), ("out", C.c_int32),
+        ("alpha", C.c_double), ("beta", C.c_double), ("clover", C.c_void_p), ("clover_mode", C.c_int32),
+        ("use_scale", C.c_int32),
+    ]
+
+
+class Operator(C.Structure):
+    """b200wd_operator: a linear operator as a program of hop stages."""
+
+    _fields_ = [
+        ("lat", Lattice), ("dtype", C.c_int32), ("n_stages", C.c_int32), ("links", C.c_void_p),
+        ("tmp", C.c_void_p), ("stage", HopStage * MAX_STAGES),
+    ]
+
+    @classmethod
+    def make(cls, lat: Lattice, dtype: int, links: int, stages, tmp: int | None = None) -> "Operator":
+        if not 1 <= len(stages) <= MAX_STAGES:
+            raise ValueError(f"operator needs 1..{MAX_STAGES} stages, got {len(stages)}")
+        op = cls()
+        op.lat = lat
+        op.dtype = int(dtype)
+        op.n_stages = len(stages)
+        op.links = links
+        op.tmp = tmp
+        for i, g in enumerate(stages):
+            st = op.stage[i]
+            st.dst_parity = int(g["dst_parity"])
+            st.src, st.xself, st.out = int(g["src"]), int(g.get("xself", OPND_NONE)), int(g["out"])
+            st.alpha, st.beta = float(g.get("alpha", 0.0)), float(g["beta"])
+            st.clover = g.get("clover")
+            st.clover_mode = int(g.get("clover_mode", 0)) if g.get("clover") else 0
+            st.use_scale = int(bool(g.get("use_scale", False)))
+        return op
+
+
 _vp, _i32, _i64, _dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
 _LAT = C.POINTER(Lattice)
 _ST = C.POINTER(GmresState)
+_OP = C.POINTER(Operator)
 
 # name -> argtypes (restype int unless noted)
 SIGNATURES = {
@@ -78,6 +120,8 @@ SIGNATURES = {
     "b200wd_gmres_mgs": [_ST, _i32, _i32, _i64, _i32, _vp, _vp, _vp, _vp],
     "b200wd_gmres_close_column": [_ST, _i32, _vp],
     "b200wd_gmres_update": [_ST, _i32, _i64, _i32, C.POINTER(_vp), _vp, _vp],
+    "b200wd_operator_apply": [_OP, _i32, _vp, _vp, _vp, _vp],
+    "b200wd_gmres_arnoldi": [_ST, _OP, _i32, _i64, C.POINTER(_vp), _vp, _vp],
 }
 RESTYPES = {"b200wd_last_error": C.c_char_p, "b200wd_reduce_scratch_bytes": _i64}
 

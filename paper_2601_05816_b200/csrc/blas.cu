@@ -506,3 +506,32 @@ extern "C" int b200wd_gmres_update(const b200wd_gmres_state* st, int32_t j_done,
       j_done, n_sites, s, zl, static_cast<double2*>(psi), gstate(st));
   return check_launch("b200wd_gmres_update");
 }
+
+extern "C" int b200wd_gmres_arnoldi(const b200wd_gmres_state* st, const b200wd_operator* op, int32_t j,
+                                    int64_t n_sites, const void* const* z, double* relnorm_host, void* stream) {
+  CHECK_STATE(st);
+  B200WD_REQUIRE(op != nullptr && z != nullptr, "NULL pointer");
+  B200WD_REQUIRE(0 <= j && j < st->m, "column %d outside restart length %d", j, st->m);
+  B200WD_REQUIRE(op->dtype == B200WD_C128, "the device GMRES runs in complex128");
+  const int32_t s = 12;
+  CHECK_FIELD(n_sites, s, st->b);
+  for (int p = 0; p <= j + 1; ++p) B200WD_REQUIRE(z[p] != nullptr, "basis pointer %d is NULL", p);
+  void* w = const_cast<void*>(z[j + 1]);
+  // w = A V_j = sigma_j A Z_j  (row j of sigma)
+  const double* sig = static_cast<const double*>(st->sigma) + (int64_t)j * st->b;
+  if (int rc = b200wd_operator_apply(op, st->b, z[j], w, sig, stream)) return rc;
+  if (int rc = b200wd_gmres_dot(st, n_sites, s, z[0], w, stream)) return rc;
+  for (int p = 0; p <= j; ++p)
+    if (int rc = b200wd_gmres_mgs(st, j, p, n_sites, s, w, z[p], p < j ? z[p + 1] : nullptr, stream)) return rc;
+  if (int rc = b200wd_gmres_close_column(st, j, stream)) return rc;
+  if (relnorm_host) {
+    cudaStream_t cs = as_stream(stream);
+    cudaError_t e = cudaMemcpyAsync(relnorm_host, st->relnorm, sizeof(double) * st->b, cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+    if (e != cudaSuccess) {
+      set_error("b200wd_gmres_arnoldi: %s", cudaGetErrorString(e));
+      return B200WD_ERR_CUDA;
+    }
+  }
+  return B200WD_OK;
+}

@@ -142,3 +142,26 @@ extern "C" int b200wd_halo_pack(const b200wd_lattice* lat, int32_t dtype, int32_
   else launch_pack_c64(p, lam_face, chi_face, st);
   return check_launch("b200wd_halo_pack");
 }
+
+extern "C" int b200wd_operator_apply(const b200wd_operator* op, int32_t b, const void* in, void* out,
+                                     const double* scale, void* stream) {
+  B200WD_REQUIRE(op != nullptr, "operator descriptor is NULL");
+  B200WD_REQUIRE(op->n_stages >= 1 && op->n_stages <= B200WD_MAX_STAGES, "operator has %d stages (1..%d)",
+                 op->n_stages, B200WD_MAX_STAGES);
+  B200WD_REQUIRE(in && out, "NULL field pointer");
+  for (int i = 0; i < op->n_stages; ++i) {
+    const b200wd_hop_stage& g = op->stage[i];
+    const void* opnd[4] = {nullptr, in, out, op->tmp};
+    B200WD_REQUIRE(g.src >= 1 && g.src <= 3 && g.out >= 1 && g.out <= 3 && g.xself >= 0 && g.xself <= 3,
+                   "stage %d: operand codes src=%d xself=%d out=%d", i, g.src, g.xself, g.out);
+    B200WD_REQUIRE(g.out != B200WD_OPND_IN, "stage %d writes the operator input", i);
+    B200WD_REQUIRE((g.src != B200WD_OPND_TMP && g.out != B200WD_OPND_TMP && g.xself != B200WD_OPND_TMP) ||
+                       op->tmp != nullptr,
+                   "stage %d uses the scratch field but tmp is NULL", i);
+    if (int rc = b200wd_hop_clover(&op->lat, op->dtype, b, g.dst_parity, op->links, opnd[g.src], opnd[g.xself],
+                                   const_cast<void*>(opnd[g.out]), g.alpha, g.beta, g.use_scale ? scale : nullptr,
+                                   0, op->lat.dims[0], nullptr, nullptr, g.clover, g.clover_mode, stream))
+      return rc;
+  }
+  return B200WD_OK;
+}

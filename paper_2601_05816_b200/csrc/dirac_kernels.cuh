@@ -544,11 +544,16 @@ static bool launch_ring_nb(const HopParams& p, int64_t nblk, int S, cudaStream_t
         return false;
       attr_smem = smem;
     }
-    int ctas_per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, hop_ring_kernel<R, V, B, NB, PAR>, Sh::NT,
-                                                      smem) != cudaSuccess ||
-        ctas_per_sm <= 0)
-      return false;
+    static int occ[9] = {0};  // CTAs per SM by ring depth, queried once
+    if (occ[S] == 0) {
+      int c = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, hop_ring_kernel<R, V, B, NB, PAR>, Sh::NT, smem) !=
+              cudaSuccess ||
+          c <= 0)
+        return false;
+      occ[S] = c;
+    }
+    const int ctas_per_sm = occ[S];
     static int sm_count = 0;
     if (sm_count == 0) {
       int dev = 0;

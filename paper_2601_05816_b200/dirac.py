@@ -146,6 +146,14 @@ class DiracOperator:
                    clover=self.clover, clover_mode=1, stream=stream)
         return out
 
+    def native_operator(self, v: DeviceField) -> "_lib.Operator":
+        """This operator as a b200wd_operator program (one hop stage), for
+        library-side drivers such as b200wd_gmres_arnoldi."""
+        stage = dict(dst_parity=-1, src=_lib.OPND_IN, xself=_lib.OPND_IN, out=_lib.OPND_OUT,
+                     alpha=4.0 + self.params.m0, beta=-1.0, use_scale=True,
+                     clover=None if self.clover is None else self.clover.ptr, clover_mode=1)
+        return _lib.Operator.make(self.lat, dtype_code(self.dtype), self.gauge.ptr, [stage])
+
     def apply_range(self, v: DeviceField, out: DeviceField, t_begin: int, t_end: int, stream=None) -> None:
         """Write only the T slices [t_begin, t_end) of out = D v."""
         hop_device(self.lat, self.dtype, v.b, -1, self.gauge, v, out, v, 4.0 + self.params.m0, -1.0, None,

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import logging
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -31,6 +32,9 @@ from .dirac import DiracOperator, DiracParams
 from .fields import BlockSpinorField
 from .oddeven import SchurOperator
 
+# B200WD_PY_ARNOLDI=1 issues the Arnoldi step kernel by kernel from Python
+# (the multi-rank path always does, to all-reduce between passes).
+NATIVE_ARNOLDI = os.environ.get("B200WD_PY_ARNOLDI", "0") != "1"
 log = logging.getLogger(__name__)
 _TINY = 1e-300
 
@@ -188,6 +192,12 @@ def gmres_solve(op, eta, psi0, cfg: GmresConfig) -> GmresResult:
         psi = upload(psi0, "c128", parity=d_eta.parity) if not isinstance(psi0, DeviceField) else psi0.copy()
     z = [d_eta.empty_like() for _ in range(m + 1)]
     zptrs = (ctypes.c_void_p * (m + 1))(*[zz.ptr for zz in z])
+    # Single rank, stencil operator: the whole Arnoldi step is issued by the
+    # library (b200wd_gmres_arnoldi), one ABI call per iteration.
+    nop = None
+    if reduce is None and not cfg.reorthogonalize and NATIVE_ARNOLDI and hasattr(dop, "native_operator"):
+        nop = dop.native_operator(z[0])
+    rel_host = torch.empty(b, dtype=torch.float64, pin_memory=True) if nop is not None else None
 
     block_norm2_device(d_eta, st.dot)
     allreduce()
@@ -211,18 +221,23 @@ def gmres_solve(op, eta, psi0, cfg: GmresConfig) -> GmresResult:
         j_done = 0
         if not finish:
             for j in range(m):
-                w = z[j + 1]
-                dop.apply_device(z[j], w, st.sigma[j])  # w = A V_j = sigma_j A Z_j
-                chk(L.b200wd_gmres_dot(st.ref, n, s, z[0].ptr, w.ptr, stream), "gmres_dot")
-                allreduce()
-                for p in range(j + 1):
-                    nxt = z[p + 1].ptr if p < j else None
-                    chk(L.b200wd_gmres_mgs(st.ref, j, p, n, s, w.ptr, z[p].ptr, nxt, stream), "gmres_mgs")
+                if nop is not None:
+                    chk(L.b200wd_gmres_arnoldi(st.ref, ctypes.byref(nop), j, n, zptrs, rel_host.data_ptr(),
+                                               stream), "gmres_arnoldi")
+                    rel = rel_host.numpy().copy()
+                else:
+                    w = z[j + 1]
+                    dop.apply_device(z[j], w, st.sigma[j])  # w = A V_j = sigma_j A Z_j
+                    chk(L.b200wd_gmres_dot(st.ref, n, s, z[0].ptr, w.ptr, stream), "gmres_dot")
                     allreduce()
-                if cfg.reorthogonalize:
-                    _reorthogonalize(st, z, j, w, reduce)
-                chk(L.b200wd_gmres_close_column(st.ref, j, stream), "gmres_close_column")
-                rel = st.relnorm.cpu().numpy().copy()
+                    for p in range(j + 1):
+                        nxt = z[p + 1].ptr if p < j else None
+                        chk(L.b200wd_gmres_mgs(st.ref, j, p, n, s, w.ptr, z[p].ptr, nxt, stream), "gmres_mgs")
+                        allreduce()
+                    if cfg.reorthogonalize:
+                        _reorthogonalize(st, z, j, w, reduce)
+                    chk(L.b200wd_gmres_close_column(st.ref, j, stream), "gmres_close_column")
+                    rel = st.relnorm.cpu().numpy().copy()
                 iterations += 1
                 history.append(rel)
                 j_done = j + 1

@@ -166,6 +166,24 @@ class SchurOperator:
             self._tmp = t
         return t
 
+    def native_operator(self, v: DeviceField):
+        """S as a two-stage b200wd_operator program (same launches as
+        apply_device); None when the operator runs over a T split."""
+        if self.comm is not None:
+            return None
+        tmp = self._tmp_like(v)
+        a = self.diag
+        I, O, T = _lib.OPND_IN, _lib.OPND_OUT, _lib.OPND_TMP
+        if self.clover_inv is None:
+            stages = [dict(dst_parity=self.elim_parity, src=I, out=T, beta=1.0 / a),
+                      dict(dst_parity=self.keep_parity, src=T, xself=I, out=O, alpha=a, beta=-1.0, use_scale=True)]
+        else:
+            stages = [dict(dst_parity=self.elim_parity, src=I, out=T, beta=1.0, clover=self.clover_inv.ptr,
+                           clover_mode=2),
+                      dict(dst_parity=self.keep_parity, src=T, xself=I, out=O, alpha=a, beta=-1.0, use_scale=True,
+                           clover=self.clover_keep.ptr, clover_mode=1)]
+        return _lib.Operator.make(self.lat, dtype_code(self.dtype), self.gauge.ptr, stages, tmp.ptr)
+
     def apply_device(self, v: DeviceField, out: DeviceField | None = None, scale=None) -> DeviceField:
         """out = scale_r * S v: two parity-restricted hop launches (oddeven.py:165-174)."""
         if v.n_sites != self.n_sites:

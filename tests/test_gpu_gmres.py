@@ -190,3 +190,62 @@ def test_tsplit_comm_single_rank_matches_single_gpu():
         r0 = P.solve_dirac(P.DiracParams(m0=0.1), gauge, None, eta, cfg, odd_even=oe)
         assert r1.iterations == r0.iterations
         assert np.all(r1.full_relnorms <= 1e-10)
+
+
+@pytest.mark.parametrize("case", ["full", "oe", "oe_clover", "full_clover"])
+def test_native_arnoldi_step_bitwise_equals_python_issued(case, monkeypatch):
+    """b200wd_gmres_arnoldi (one ABI call per iteration) launches the same
+    kernels in the same order as the Python-issued step: identical bits."""
+    import paper_2601_05816_b200.gmres as G
+    dims = (8, 4, 4, 4)
+    geom = P.LatticeGeometry(dims)
+    links = O.flip_time_boundary(O.near_unit_gauge(dims, 0.3, 11), dims)
+    clover = None
+    if case.endswith("clover"):
+        clover = P.CloverField(geom, O.pack_clover(O.gen_clover_random(dims, 0.05, 3)))
+    eta = host_field(O.gen_spinor(512, 4, 13), 2, geom)
+    cfg = P.GmresConfig(restart_len=12, restarts=20, tol=1e-10)
+    runs = []
+    for native in (True, False):
+        monkeypatch.setattr(G, "NATIVE_ARNOLDI", native)
+        runs.append(P.solve_dirac(P.DiracParams(m0=0.1), P.GaugeField(geom, links), clover, eta, cfg,
+                                  odd_even=case.startswith("oe")))
+    a, b = runs
+    assert a.iterations == b.iterations
+    assert np.array_equal(np.array(a.result.history), np.array(b.result.history))
+    assert np.array_equal(a.psi.ksi(), b.psi.ksi())
+    assert np.all(a.full_relnorms <= 1e-10)
+
+
+def test_operator_apply_matches_apply_device():
+    """b200wd_operator_apply of the stage programs == the Python-issued applies."""
+    import ctypes
+    import torch
+    from paper_2601_05816_b200 import _lib
+    from paper_2601_05816_b200.device import stream_ptr, upload
+    dims = (8, 4, 4, 8)
+    geom = P.LatticeGeometry(dims)
+    gauge = P.GaugeField(geom, O.gen_gauge_random(dims, 5))
+    clover = P.CloverField(geom, O.pack_clover(O.gen_clover_random(dims, 0.05, 4)))
+    for dtype in ("c128", "c64"):
+        for cl in (None, clover):
+            op = P.DiracOperator(P.DiracParams(m0=0.2), gauge, cl, dtype)
+            v = upload(host_field(O.gen_spinor(geom.n_sites, 6, 2), 2, geom), dtype)
+            scale = torch.linspace(0.5, 1.5, 6, dtype=torch.float64, device="cuda")
+            ref = op.apply_device(v, None, scale)
+            out = v.empty_like()
+            nop = op.native_operator(v)
+            _lib.call("b200wd_operator_apply", ctypes.byref(nop), 6, v.ptr, out.ptr, scale.data_ptr(), stream_ptr())
+            assert torch.equal(out.data, ref.data)
+            for keep in (0, 1):
+                so = P.SchurOperator(P.DiracParams(m0=0.2), gauge, cl, keep_parity=keep, dtype=dtype)
+                ve = upload(host_field(O.gen_spinor(geom.n_sites // 2, 6, 3), 2), dtype, parity=keep)
+                ref = so.apply_device(ve, None, scale)
+                out = ve.empty_like()
+                nop = so.native_operator(ve)
+                _lib.call("b200wd_operator_apply", ctypes.byref(nop), 6, ve.ptr, out.ptr, scale.data_ptr(),
+                          stream_ptr())
+                assert torch.equal(out.data, ref.data)
+    bad = _lib.Operator()
+    with pytest.raises(ValueError):
+        _lib.call("b200wd_operator_apply", ctypes.byref(bad), 6, v.ptr, out.ptr, None, stream_ptr())
