@@ -15,7 +15,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libb200wd.so"
-SOURCES = ["capi.cu", "layout.cu", "dirac.cu", "dirac_c128.cu", "dirac_c64.cu", "blas.cu"]
+SOURCES = ["capi.cu", "layout.cu", "dirac.cu", "dirac_c128.cu", "dirac_c64.cu", "blas.cu"] + [
+    f"dirac_{d}_{g}.cu" for d in ("c128", "c64") for g in ("b0", "b4", "b8", "b16", "b24")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

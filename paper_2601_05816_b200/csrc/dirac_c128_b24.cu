@@ -1,0 +1,8 @@
+// c128 hopping-kernel instantiations, rhs counts [24, 32] (separate unit: parallel build)
+#define B200WD_HOP_ENTRY_DEF
+#include "dirac_kernels.cuh"
+
+namespace b200wd {
+template void hop_entry<double, 1, 24>(const HopParams&, cudaStream_t);
+template void hop_entry<double, 1, 32>(const HopParams&, cudaStream_t);
+}  // namespace b200wd

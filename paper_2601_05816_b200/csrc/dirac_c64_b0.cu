@@ -1,0 +1,11 @@
+// c64 hopping-kernel instantiations, rhs counts [0, 1, 2, 3] (separate unit: parallel build)
+#define B200WD_HOP_ENTRY_DEF
+#include "dirac_kernels.cuh"
+
+namespace b200wd {
+template void hop_entry<float, 1, 0>(const HopParams&, cudaStream_t);
+template void hop_entry<float, 1, 1>(const HopParams&, cudaStream_t);
+template void hop_entry<float, 1, 3>(const HopParams&, cudaStream_t);
+template void hop_entry<float, 2, 0>(const HopParams&, cudaStream_t);
+template void hop_entry<float, 2, 2>(const HopParams&, cudaStream_t);
+}  // namespace b200wd

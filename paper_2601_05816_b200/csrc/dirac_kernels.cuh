@@ -272,12 +272,30 @@ __device__ __forceinline__ int64_t z_neighbor(int64_t d, int z, int Z, int step)
   return (z == 0) ? d + (Z - 1) : d - 1;
 }
 
+// Item index in traversal order -> item index in natural order (relative to
+// d_begin).  Items are NB field blocks; lz items per z line.
+__device__ __forceinline__ int64_t item_nat(int64_t it, const HopParams& p, uint32_t lz) {
+  if (p.tile_x == 0) return it;
+  uint32_t i = (uint32_t)it;
+  const uint32_t zi = i % lz;
+  i /= lz;
+  const uint32_t tl = (uint32_t)(p.tile_x * p.tile_y);
+  const uint32_t q = i % tl;
+  i /= tl;
+  const uint32_t t = i % (uint32_t)p.tile_nt;
+  const uint32_t tile = i / (uint32_t)p.tile_nt;
+  const uint32_t ny = (uint32_t)(p.Y / p.tile_y);
+  const uint32_t x = (tile / ny) * p.tile_x + q / p.tile_y;
+  const uint32_t y = (tile % ny) * p.tile_y + q % p.tile_y;
+  return (((int64_t)t * p.X + x) * p.Y + y) * lz + zi;
+}
+
 // tile H in 0..5: hop (mu = H/2, forward if H even); H == 6: own blocks (z tile).
 // PAR: checkerboard fields (a field block of 8 cb sites = 16 natural sites of
 // one z line, Z % 16 == 0); links are always natural-site blocks.
 template <typename R, int V, int B, int NB, bool PAR, int H>
 __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, const BlkCoord& c0, cx<R>* slot,
-                                           uint64_t* full) {
+                                           uint64_t* full, uint64_t pol_first, uint64_t pol_t1) {
   using C = cx<R>;
   using Sh = RingShape<R, V, B, NB, PAR>;
   constexpr int F = Sh::F;
@@ -303,7 +321,12 @@ __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, cons
       }
     }
     if (contiguous) {
-      bulk_g2s(slot, src + nb0 * 96 * B, Sh::SPIN * sizeof(C), full);
+      if (H == 1)  // t-1 neighbour: the last use of these blocks in either order
+        bulk_g2s_hint(slot, src + nb0 * 96 * B, Sh::SPIN * sizeof(C), full, pol_first);
+      else if (H == 0 && p.hint_t1)  // t+1 neighbour: first touch
+        bulk_g2s_hint(slot, src + nb0 * 96 * B, Sh::SPIN * sizeof(C), full, pol_t1);
+      else
+        bulk_g2s(slot, src + nb0 * 96 * B, Sh::SPIN * sizeof(C), full);
       bulk_g2s(slot + Sh::SPIN, U + (MU * nblk + F * (FWD ? gb0 : nb0)) * 72, NB * Sh::LPB * sizeof(C), full);
     } else {
       BlkCoord c = c0;
@@ -319,7 +342,9 @@ __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, cons
   }
 }
 
-template <typename R, int V, int B, int NB, bool PAR>
+// TILED: patched traversal order (checkerboard fields).  ZG: items are not
+// whole z lines, the z hops at the item edges read global memory.
+template <typename R, int V, int B, int NB, bool PAR, bool TILED, bool ZG>
 __global__ void __launch_bounds__(RingShape<R, V, B, NB, PAR>::NT) hop_ring_kernel(const HopParams p,
                                                                                    int64_t n_items, int S) {
   using C = cx<R>;
@@ -344,16 +369,21 @@ __global__ void __launch_bounds__(RingShape<R, V, B, NB, PAR>::NT) hop_ring_kern
   if (tid >= Sh::NC) {
     if (tid == Sh::NC) {  // one elected lane issues every copy
       int pslot = 0, pfirst = 1;
+      const uint64_t pol_first = l2_evict_first_policy();
+      // t+1 blocks come back as own blocks one patch slice later (tiled) or
+      // after a whole T slice (natural order: no reuse to protect)
+      const uint64_t pol_t1 = p.hint_t1 == 2 ? l2_evict_last_policy() : pol_first;
       uint32_t pphase = 0;  // phase of the next fill of pslot; its release is phase^1 of empty
+      const uint32_t lz = (uint32_t)(p.Z / (8 * F * NB));
       for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int64_t gb0 = (p.d_begin >> 3) + it * NB;
+        const int64_t gb0 = (p.d_begin >> 3) + (TILED ? item_nat(it, p, lz) : it) * NB;
         const BlkCoord c0 = block_coord(gb0 * 8 * F, p);
 #if B200WD_L2_PREFETCH
         {  // warm L2 with the compulsory misses of a later item of this CTA:
            // its t+1 neighbour blocks (first touch in sweep order) and links
           const int64_t nx = it + (int64_t)B200WD_L2_PREFETCH * gridDim.x;
           if (nx < n_items) {
-            const int64_t gn = (p.d_begin >> 3) + nx * NB;
+            const int64_t gn = (p.d_begin >> 3) + (TILED ? item_nat(nx, p, lz) : nx) * NB;
             const BlkCoord cn = block_coord(gn * 8 * F, p);
             const int64_t nb = block_neighbor<0, true>(gn * 8 * F, cn, p) / (8 * F);
             const C* srcp = static_cast<const C*>(p.src);
@@ -368,7 +398,7 @@ __global__ void __launch_bounds__(RingShape<R, V, B, NB, PAR>::NT) hop_ring_kern
 #define B200WD_PRODUCE(H)                                                                   \
   {                                                                                         \
     if (pfirst == 0) mbar_wait(&empty[pslot], pphase ^ 1u);                                 \
-    ring_issue<R, V, B, NB, PAR, H>(p, gb0, c0, ring + pslot * Sh::SLOT, &full[pslot]);   \
+    ring_issue<R, V, B, NB, PAR, H>(p, gb0, c0, ring + pslot * Sh::SLOT, &full[pslot], pol_first, pol_t1); \
     if (++pslot == S) {                                                                     \
       pslot = 0;                                                                            \
       pphase ^= 1u;                                                                         \
@@ -406,8 +436,11 @@ __global__ void __launch_bounds__(RingShape<R, V, B, NB, PAR>::NT) hop_ring_kern
 
   int cslot = 0;
   uint32_t cphase = 0;
+  const uint32_t lz = (uint32_t)(p.Z / (8 * F * NB));
   for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
-    const int64_t gb0 = (p.d_begin >> 3) + it * NB;
+    // natural order keeps gb0 affine in `it`: a separate instantiation,
+    // the compiler schedules that loop markedly better (tools/bench_strong.py)
+    const int64_t gb0 = (p.d_begin >> 3) + (TILED ? item_nat(it, p, lz) : it) * NB;
     const int64_t d = (gb0 + j) * 8 + lo;  // field index of this thread's site
     // natural site: full lattice d; checkerboard 2d + (parity fix of the block's line)
     int64_t xn = d;
@@ -441,28 +474,52 @@ __global__ void __launch_bounds__(RingShape<R, V, B, NB, PAR>::NT) hop_ring_kern
           for (int k = 0; k < 12; ++k) acc[v][k] = mk(R(0), R(0));
       }
       const int z = (int)((uint32_t)xn % (uint32_t)Z);
-      {
-        const int64_t xp = z_neighbor(xn, z, Z, 1);
-        const int64_t fi = PAR ? (xp >> 1) : xp;
-        const int64_t jb = (fi >> 3) - gb0;
-        const C* ul = zt + Sh::SPIN + lofs;  // U_3(x), own blocks
-        if (jb >= 0 && jb < NB)
-          hop_full<3, true, R, V, true, true>(acc, zt + jb * 96 * B + (fi & 7) * B + r0, KST, ul, 8);
-        else
-          hop_full<3, true, R, V, false, true>(acc, src + spinor_base(fi, 12, B) + r0, KST, ul, 8);
-      }
-      {
-        const int64_t xp = z_neighbor(xn, z, Z, -1);
-        const int64_t fi = PAR ? (xp >> 1) : xp;
-        const int64_t jb = (fi >> 3) - gb0;
-        const int lj = (int)(xp - nat0);
-        const bool lin = lj >= 0 && lj < 8 * F * NB;
-        if (jb >= 0 && jb < NB && lin)
-          hop_full<3, false, R, V, true, true>(acc, zt + jb * 96 * B + (fi & 7) * B + r0, KST,
-                                               zt + Sh::SPIN + (lj >> 3) * 72 + (lj & 7), 8);
-        else
-          hop_full<3, false, R, V, false, false>(acc, src + spinor_base(fi, 12, B) + r0, KST,
-                                                 U + link_base(xp, 3, nblk), 8);
+      if constexpr (ZG) {
+        // z hops through generic pointers (shared memory inside the item, global
+        // memory at its z edges): one branch-free load batch per hop
+        {
+          const int64_t xp = z_neighbor(xn, z, Z, 1);
+          const int64_t fi = PAR ? (xp >> 1) : xp;
+          const int64_t jb = (fi >> 3) - gb0;
+          const C* sp = (jb >= 0 && jb < NB) ? zt + jb * 96 * B + (fi & 7) * B + r0
+                                             : src + spinor_base(fi, 12, B) + r0;
+          hop_full<3, true, R, V, true, true>(acc, sp, KST, zt + Sh::SPIN + lofs, 8);
+        }
+        {
+          const int64_t xp = z_neighbor(xn, z, Z, -1);
+          const int64_t fi = PAR ? (xp >> 1) : xp;
+          const int64_t jb = (fi >> 3) - gb0;
+          const int lj = (int)(xp - nat0);
+          const C* sp = (jb >= 0 && jb < NB) ? zt + jb * 96 * B + (fi & 7) * B + r0
+                                             : src + spinor_base(fi, 12, B) + r0;
+          const C* up = (lj >= 0 && lj < 8 * F * NB) ? zt + Sh::SPIN + (lj >> 3) * 72 + (lj & 7)
+                                                     : U + link_base(xp, 3, nblk);
+          hop_full<3, false, R, V, true, true>(acc, sp, KST, up, 8);
+        }
+      } else {
+        {
+          const int64_t xp = z_neighbor(xn, z, Z, 1);
+          const int64_t fi = PAR ? (xp >> 1) : xp;
+          const int64_t jb = (fi >> 3) - gb0;
+          const C* ul = zt + Sh::SPIN + lofs;  // U_3(x), own blocks
+          if (jb >= 0 && jb < NB)
+            hop_full<3, true, R, V, true, true>(acc, zt + jb * 96 * B + (fi & 7) * B + r0, KST, ul, 8);
+          else
+            hop_full<3, true, R, V, false, true>(acc, src + spinor_base(fi, 12, B) + r0, KST, ul, 8);
+        }
+        {
+          const int64_t xp = z_neighbor(xn, z, Z, -1);
+          const int64_t fi = PAR ? (xp >> 1) : xp;
+          const int64_t jb = (fi >> 3) - gb0;
+          const int lj = (int)(xp - nat0);
+          const bool lin = lj >= 0 && lj < 8 * F * NB;
+          if (jb >= 0 && jb < NB && lin)
+            hop_full<3, false, R, V, true, true>(acc, zt + jb * 96 * B + (fi & 7) * B + r0, KST,
+                                                 zt + Sh::SPIN + (lj >> 3) * 72 + (lj & 7), 8);
+          else
+            hop_full<3, false, R, V, false, false>(acc, src + spinor_base(fi, 12, B) + r0, KST,
+                                                   U + link_base(xp, 3, nblk), 8);
+        }
       }
       __syncwarp();
       if (lead) mbar_arrive(&empty[slot]);
@@ -525,46 +582,118 @@ static RingCfg ring_env() {
   return c;
 }
 
+// A T slice of the source field larger than this is not reused from L2 by
+// the t+1 hop of the next slice (tools/bench_strong.py on 48^3 x 96).
+constexpr int64_t kSliceNoReuse = 48ll << 20;
+
+// L2 budget for one T slice of a traversal patch (B200WD_TILE_KB, default
+// 24 MB; 0 = natural order everywhere).  The patch's t-1, t and t+1 slices
+// (~3x this) must stay resident next to the streaming output and links.
+static int64_t tile_budget() {
+  static int64_t kb = -1;
+  if (kb < 0) {
+    const char* e = getenv("B200WD_TILE_KB");
+    kb = e ? atoll(e) : 24 * 1024;
+  }
+  return kb << 10;
+}
+
+// Patch the traversal order when one T slice of the source field does not
+// fit the budget: the largest tile_x | X, tile_y | Y patch (most nearly square)
+// whose slice fits.  Needs whole z lines per item set and slice-aligned ranges.
+static void choose_tiles(HopParams& p, int F, int NB, size_t bytes_per_field_site) {
+  p.tile_x = p.tile_y = p.tile_nt = 0;
+  const int64_t budget = tile_budget();
+  if (budget <= 0 || p.Z % (8 * F * NB)) return;
+  const int64_t per_t_field = p.per_t / F;
+  if (p.d_begin % per_t_field || p.d_end % per_t_field) return;
+  const int64_t line_bytes = (int64_t)(p.Z / F) * (int64_t)bytes_per_field_site;
+  if ((int64_t)p.X * p.Y * line_bytes <= budget) return;
+  int best_x = 0, best_y = 0;
+  double best = 1e30;
+  for (int tx = 1; tx <= p.X; ++tx) {
+    if (p.X % tx) continue;
+    for (int ty = 1; ty <= p.Y; ++ty) {
+      if (p.Y % ty || (int64_t)tx * ty * line_bytes > budget) continue;
+      const double perim = 1.0 / tx + 1.0 / ty;  // re-read fraction of the x/y neighbours
+      if (perim < best - 1e-12) {
+        best = perim;
+        best_x = tx;
+        best_y = ty;
+      }
+    }
+  }
+  if (best_x == 0 || (best_x == p.X && best_y == p.Y)) return;
+  p.tile_x = best_x;
+  p.tile_y = best_y;
+  p.tile_nt = (int32_t)((p.d_end - p.d_begin) / per_t_field);
+}
+
+template <int NB>
+static int64_t n_items_of(int64_t nblk) { return nblk / NB; }
+
+template <typename R, int V, int B, int NB, bool PAR, bool TILED, bool ZG>
+static bool launch_ring_kernel(const HopParams& p, int64_t n_items, int S, size_t smem, cudaStream_t st) {
+  using Sh = RingShape<R, V, B, NB, PAR>;
+  static size_t attr_smem = 0;
+  if (attr_smem < smem) {
+    if (cudaFuncSetAttribute(hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return false;
+    attr_smem = smem;
+  }
+  static int occ[9] = {0};  // CTAs per SM by ring depth, queried once
+  if (occ[S] == 0) {
+    int c = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG>, Sh::NT,
+                                                      smem) !=
+            cudaSuccess ||
+        c <= 0)
+      return false;
+    occ[S] = c;
+  }
+  static int sm_count = 0;
+  if (sm_count == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int64_t grid = (int64_t)occ[S] * sm_count;
+  if (grid > n_items) grid = n_items;
+  hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG><<<(unsigned)grid, Sh::NT, smem, st>>>(p, n_items, S);
+  return true;
+}
+
 template <typename R, int V, int B, int NB, bool PAR>
-static bool launch_ring_nb(const HopParams& p, int64_t nblk, int S, cudaStream_t st) {
+static bool launch_ring_nb(const HopParams& p_in, int64_t nblk, int S, cudaStream_t st) {
   using Sh = RingShape<R, V, B, NB, PAR>;
   if constexpr (!Sh::valid) {
     return false;
   } else {
     if (nblk % NB) return false;
+    HopParams p = p_in;
+    const size_t site_bytes = (size_t)12 * B * sizeof(cx<R>);
+    // patched order for checkerboard fields only: measured +2-6% on the Schur
+    // hops of 32^3 x 64 (tools/variants_cmp.sh), but slower than the natural
+    // order for the full-lattice apply on 48^3 x 96
+    if (PAR) choose_tiles(p, Sh::F, NB, site_bytes);
+    const int64_t slice_bytes = (int64_t)(p.per_t / Sh::F) * (int64_t)site_bytes;
+    p.hint_t1 = p.tile_x ? 2 : (slice_bytes > kSliceNoReuse ? 1 : 0);
+    const bool whole_lines = (8 * Sh::F * NB) % p.Z == 0;
     if (S <= 0) S = (Sh::SLOT_BYTES >= 40 * 1024) ? (200 * 1024) / Sh::SLOT_BYTES : (100 * 1024) / Sh::SLOT_BYTES;
     if (S < 2) S = 2;
     if (S > 8) S = 8;
     size_t smem = Sh::smem(S);
     while (smem > 227 * 1024 && S > 2) smem = Sh::smem(--S);
-    static size_t attr_smem = 0;
-    if (attr_smem < smem) {
-      if (cudaFuncSetAttribute(hop_ring_kernel<R, V, B, NB, PAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem) != cudaSuccess)
-        return false;
-      attr_smem = smem;
+    const int64_t ni = n_items_of<NB>(nblk);
+    if constexpr (PAR) {
+      if (p.tile_x) {
+        if (whole_lines) return launch_ring_kernel<R, V, B, NB, PAR, true, false>(p, ni, S, smem, st);
+        return launch_ring_kernel<R, V, B, NB, PAR, true, true>(p, ni, S, smem, st);
+      }
     }
-    static int occ[9] = {0};  // CTAs per SM by ring depth, queried once
-    if (occ[S] == 0) {
-      int c = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, hop_ring_kernel<R, V, B, NB, PAR>, Sh::NT, smem) !=
-              cudaSuccess ||
-          c <= 0)
-        return false;
-      occ[S] = c;
-    }
-    const int ctas_per_sm = occ[S];
-    static int sm_count = 0;
-    if (sm_count == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const int64_t n_items = nblk / NB;
-    int64_t grid = (int64_t)ctas_per_sm * sm_count;
-    if (grid > n_items) grid = n_items;
-    hop_ring_kernel<R, V, B, NB, PAR><<<(unsigned)grid, Sh::NT, smem, st>>>(p, n_items, S);
-    return true;
+    if (whole_lines) return launch_ring_kernel<R, V, B, NB, PAR, false, false>(p, ni, S, smem, st);
+    return launch_ring_kernel<R, V, B, NB, PAR, false, true>(p, ni, S, smem, st);
   }
 }
 
@@ -777,13 +906,22 @@ template <typename R, int V> __host__ __device__ constexpr bool wanted_b(int bb)
   return bb % V == 0 && (V == 2 || sizeof(R) == 8 || bb % 2 == 1);
 }
 
+// One entry point per (R, V, B), defined (B200WD_HOP_ENTRY_DEF) and explicitly
+// instantiated in the dirac_c*_b*.cu units so the builds run in parallel.
+template <typename R, int V, int B> void hop_entry(const HopParams& p, cudaStream_t st);
+#ifdef B200WD_HOP_ENTRY_DEF
+template <typename R, int V, int B> void hop_entry(const HopParams& p, cudaStream_t st) {
+  launch_hop_b<R, V, B>(p, st);
+}
+#endif
+
 template <typename R, int V>
 static void launch_hop(const HopParams& p, cudaStream_t st) {
   switch (p.b) {
 #define B200WD_CASE(BB)                       \
   case BB:                                    \
     if constexpr (wanted_b<R, V>(BB)) {       \
-      launch_hop_b<R, V, BB>(p, st);          \
+      hop_entry<R, V, BB>(p, st);             \
       return;                                 \
     }                                         \
     break;
@@ -801,7 +939,7 @@ static void launch_hop(const HopParams& p, cudaStream_t st) {
     default:
       break;
   }
-  launch_hop_b<R, V, 0>(p, st);
+  hop_entry<R, V, 0>(p, st);
 }
 
 template <typename R, int V>

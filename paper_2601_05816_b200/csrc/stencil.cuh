@@ -40,6 +40,15 @@ struct HopParams {
   // out = s (alpha x - M x + beta H src); mode 2: out = s M (alpha x + beta H src)
   const void* clov;
   int32_t clov_mode;
+  // ring-kernel traversal order (0 = natural site order): items sweep the T
+  // slices of one tile_x x tile_y patch of z lines before the next patch, so
+  // the t-1 / t / t+1 slices of the patch stay in L2 (lattices whose T slice
+  // is larger than L2).  tile_nt = slices in [d_begin, d_end).
+  int32_t tile_x, tile_y, tile_nt;
+  // L2 policy of the t+1 neighbour tile copies: 0 default, 1 evict-first (a T
+  // slice exceeds L2: no reuse before eviction), 2 evict-last (patched order:
+  // the blocks return as own blocks one patch slice later)
+  int32_t hint_t1;
 };
 
 // y = M t for the two packed Hermitian 6x6 blocks of one site (fields.py:212-247:

@@ -123,3 +123,11 @@ def test_compute_paths_fail_loudly_without_gpu():
         P.apply_dirac(P.DiracParams(), P.gen_gauge(g, "unit"), None, psi)
     with pytest.raises(B200Unavailable):
         P.block_norms(psi)
+
+
+def test_near_unit_links_forked_workers_same_bits():
+    from paper_2601_05816_b200.fields import near_unit_links
+    dims = (6, 4, 4, 2)
+    ref = near_unit_links(dims, 0.3, 5)
+    assert np.array_equal(near_unit_links(dims, 0.3, 5, workers=4), ref)
+    assert np.array_equal(near_unit_links(dims, 0.3, 5, 1, 5, workers=3), ref[32:160])

@@ -1,0 +1,139 @@
+"""BASELINE configs[4]: 48^3 x 96 (10.6M sites), nrhs=12, T split over the ranks.
+
+    python tools/bench_strong.py [--gmres]                       # 1 GPU
+    torchrun --nproc-per-node N tools/bench_strong.py            # N GPUs
+
+D_W apply in complex128 and complex64 at every rank count (strong scaling:
+the global lattice is fixed, each rank owns 96/N T slices), time = max over
+ranks of CUDA-event time per apply.  With --gmres also the odd-even batched
+GMRES(8) to relative tolerance 1e-8 (the Schur system on a Gaussian
+even-parity rhs; the configs run it on 8 GPUs, here on however many ranks
+there are).  Links: near-unit SU(3), eps = 0.3, generated per T slab with
+forked workers (same bits as the serial generator).  Prints one JSON line per
+measurement.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+
+import paper_2601_05816_b200 as P  # noqa: E402
+from paper_2601_05816_b200.device import DeviceField  # noqa: E402
+from paper_2601_05816_b200.dirac import compulsory_bytes_per_site  # noqa: E402
+
+GDIMS = (96, 48, 48, 48)
+M0 = 0.1
+
+
+def hbm_peak():
+    pk = Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"
+    return float(json.loads(pk.read_text())["hbm_gbs"]) if pk.exists() else 7672.0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--b", type=int, default=12)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--dtypes", default="c128,c64")
+    ap.add_argument("--gmres", action="store_true")
+    ap.add_argument("--dims", type=int, nargs=4, default=list(GDIMS))
+    a = ap.parse_args()
+    gdims = tuple(a.dims)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = 0
+    comm = None
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+        rank = dist.get_rank()
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        from paper_2601_05816_b200.tsplit import TSplitComm
+        comm = TSplitComm(P.LatticeGeometry(gdims))
+        lg, t0 = comm.local_geom, comm.t_origin
+    else:
+        lg, t0 = P.LatticeGeometry(gdims), 0
+    dev = torch.device("cuda", torch.cuda.current_device())
+    tg = time.perf_counter()
+    links = P.near_unit_links(gdims, 0.3, 0, t0, t0 + lg.dims[0], workers=max(1, (os.cpu_count() or 1) // world))
+    gauge = P.flip_time_boundary(P.GaugeField(lg, links), gdims[0], t0)
+    del links
+    gen_s = time.perf_counter() - tg
+    n, b = lg.n_sites, a.b
+    peak = hbm_peak()
+
+    def timed(fn):
+        for _ in range(a.warmup):
+            fn()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) * 1e-3 / a.steps], device=dev, dtype=torch.float64)
+        if dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for dt in a.dtypes.split(","):
+        tdt = torch.complex128 if dt == "c128" else torch.complex64
+        g = torch.Generator(device=dev).manual_seed(rank)
+        psi = DeviceField(torch.randn((n // 8, 12, 8, b), dtype=tdt, device=dev, generator=g), n, lg)
+        eta = psi.empty_like()
+        if comm is not None:
+            comm.bind(P.DiracParams(m0=M0), gauge, None, dt)
+            t = timed(lambda: comm.apply_device(psi, eta))
+        else:
+            op = P.DiracOperator(P.DiracParams(m0=M0), gauge, None, dt)
+            t = timed(lambda: op.apply_device(psi, eta))
+        alg = compulsory_bytes_per_site(b, dt) * n
+        if rank == 0:
+            print(json.dumps({
+                "config": "BASELINE configs[4] D_W apply (strong scaling)", "lattice": list(gdims),
+                "local": list(lg.dims), "n_gpus": world, "nrhs": b, "dtype": dt, "ms_per_apply": t * 1e3,
+                "site_rhs_per_s": world * n * b / t, "hbm_gbs_per_gpu": alg / t / 1e9,
+                "frac_per_gpu": alg / t / 1e9 / peak, "link_gen_s": gen_s}), flush=True)
+        del psi, eta
+        torch.cuda.empty_cache()
+
+    if a.gmres:
+        from paper_2601_05816_b200.oddeven import SchurOperator
+        if comm is not None:
+            op = comm.schur(P.DiracParams(m0=M0), gauge, None)
+        else:
+            op = SchurOperator(P.DiracParams(m0=M0), gauge, None, keep_parity=0)
+        ne = n // 2
+        g = torch.Generator(device=dev).manual_seed(100 + rank)
+        eta_e = DeviceField(torch.randn((ne // 8, 12, 8, b), dtype=torch.complex128, device=dev, generator=g),
+                            ne, lg, 0)
+        cfg = P.GmresConfig(restart_len=8, restarts=250, tol=1e-8)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t1 = time.perf_counter()
+        res = P.gmres_solve(op, eta_e, None, cfg)
+        torch.cuda.synchronize()
+        tts = time.perf_counter() - t1
+        if rank == 0:
+            print(json.dumps({
+                "config": "BASELINE configs[4] odd-even batched GMRES(8), tol 1e-8 (Schur system)",
+                "lattice": list(gdims), "n_gpus": world, "nrhs": b, "iterations": res.iterations,
+                "time_to_solution_s": tts, "ms_per_iteration": tts / max(res.iterations, 1) * 1e3,
+                "converged": bool(res.converged.all()), "final_relnorm_max": float(res.final_relnorms.max()),
+                "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9}), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
