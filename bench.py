@@ -14,8 +14,10 @@ is one D_W apply of one nrhs block; steps rotate through enough distinct
 exceed 4x the L2 size (no L2 reuse across steps).  Batched GMRES
 time-to-solution on BASELINE configs[3] (24^3 x 48, nrhs=12, near-unit
 links, antiperiodic T, GMRES(30), tol 1e-10, full and odd-even) is added
-under "gmres" and the configs[2] Schur apply (32^3 x 64, nrhs=12, c128)
-under "schur", unless --no-gmres.
+under "gmres", the configs[2] Schur apply (32^3 x 64, nrhs=12, c128)
+under "schur" and the configs[4] apply at one GPU (48^3 x 96, nrhs=12, c128
+and c64; the strong-scaling base point, tools/bench_strong.py runs the N-rank
+split) under "strong_base", unless --no-gmres.
 """
 
 from __future__ import annotations
@@ -393,6 +395,8 @@ def main():
         sys.path.insert(0, str(ROOT / "tools"))
         from bench_schur import schur_bench
         line["schur"] = schur_bench()  # BASELINE configs[2]: 32^3x64 Schur apply, nrhs=12, c128
+        from bench_strong import single_gpu_apply
+        line["strong_base"] = single_gpu_apply()  # BASELINE configs[4] at N=1: 48^3x96, nrhs=12
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample()
     print(json.dumps(line))

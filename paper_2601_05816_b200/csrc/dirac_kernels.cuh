@@ -673,9 +673,10 @@ static bool launch_ring_nb(const HopParams& p_in, int64_t nblk, int S, cudaStrea
     if (nblk % NB) return false;
     HopParams p = p_in;
     const size_t site_bytes = (size_t)12 * B * sizeof(cx<R>);
-    // patched order for checkerboard fields only: measured +2-6% on the Schur
-    // hops of 32^3 x 64 (tools/variants_cmp.sh), but slower than the natural
-    // order for the full-lattice apply on 48^3 x 96
+    // patched order for checkerboard fields only: measured +2-8% on the Schur
+    // hops of 32^3 x 64 (tools/variants_cmp.sh); for the full-lattice apply on
+    // 48^3 x 96 every patch shape tried (1..8 x 48, 48 x 2..8, 6 x 12) was
+    // 10-25% slower than the natural order
     if (PAR) choose_tiles(p, Sh::F, NB, site_bytes);
     const int64_t slice_bytes = (int64_t)(p.per_t / Sh::F) * (int64_t)site_bytes;
     p.hint_t1 = p.tile_x ? 2 : (slice_bytes > kSliceNoReuse ? 1 : 0);

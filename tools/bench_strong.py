@@ -35,6 +35,40 @@ def hbm_peak():
     return float(json.loads(pk.read_text())["hbm_gbs"]) if pk.exists() else 7672.0
 
 
+def single_gpu_apply(gdims=GDIMS, dtypes=("c128", "c64"), b=12, steps=10, warmup=3):
+    """configs[4] at N=1 (the strong-scaling base point): D_W apply records."""
+    geom = P.LatticeGeometry(tuple(gdims))
+    tg = time.perf_counter()
+    gauge = P.flip_time_boundary(P.GaugeField(geom, P.near_unit_links(gdims, 0.3, 0, workers=os.cpu_count() or 1)))
+    gen_s = time.perf_counter() - tg
+    n, peak, out = geom.n_sites, hbm_peak(), []
+    for dt in dtypes:
+        tdt = torch.complex128 if dt == "c128" else torch.complex64
+        g = torch.Generator(device="cuda").manual_seed(0)
+        psi = DeviceField(torch.randn((n // 8, 12, 8, b), dtype=tdt, device="cuda", generator=g), n, geom)
+        eta = psi.empty_like()
+        op = P.DiracOperator(P.DiracParams(m0=M0), gauge, None, dt)
+        for _ in range(warmup):
+            op.apply_device(psi, eta)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            op.apply_device(psi, eta)
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) * 1e-3 / steps
+        alg = compulsory_bytes_per_site(b, dt) * n
+        out.append({"dtype": dt, "nrhs": b, "ms": round(t * 1e3, 4), "site_rhs_per_s": n * b / t,
+                    "hbm_gbs": round(alg / t / 1e9, 1), "frac": round(alg / t / 1e9 / peak, 4)})
+        del psi, eta, op
+    from paper_2601_05816_b200.device import gauge_cache
+    gauge_cache.clear()
+    torch.cuda.empty_cache()
+    return {"workload": "BASELINE configs[4] at 1 GPU (strong-scaling base point)", "lattice": list(gdims),
+            "records": out, "link_gen_s": round(gen_s, 2), "l2": "fields 24.5 GB (c128) >> L2"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--b", type=int, default=12)
