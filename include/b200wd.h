@@ -214,7 +214,7 @@ int b200wd_gmres_update(const b200wd_gmres_state* st, int32_t j_done, int64_t n_
 /* ---- operator programs and the native Arnoldi step ---------------------- */
 /* A linear operator as a short program of hop stages, so the library can
  * apply it without a round trip through the host language (the reference's
- * LinearOperator protocol, operator.py:1-40).  Each stage is one
+ * operator callables, gmres.py:335-339 dirac_op and oddeven.py:165-174).  Each stage is one
  * b200wd_hop_clover launch over all local slices; its src / xself / out are
  * picked from the call's input (B200WD_OPND_IN), output (B200WD_OPND_OUT) or
  * the program's scratch field `tmp` (B200WD_OPND_TMP).  The call's `scale`
@@ -253,7 +253,7 @@ typedef struct b200wd_operator {
 int b200wd_operator_apply(const b200wd_operator* op, int32_t b, const void* in, void* out,
                           const double* scale, void* stream);
 
-/* One whole Arnoldi step of column j on a single rank (gmres.py:108-157):
+/* One whole Arnoldi step of column j on a single rank (gmres.py:115-157):
  * Z_{j+1} = sigma_j op(Z_j), the fused MGS sweep against Z_0..Z_j, the column
  * close (breakdown test, Givens rotation, relnorm), then the relnorm of every
  * rhs is copied into relnorm_host (b doubles, pinned host memory) and the
