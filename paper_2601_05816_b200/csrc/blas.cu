@@ -12,10 +12,13 @@
 // one thread per rhs (gmres.py:101-177).
 #include <math.h>
 
+#include <cooperative_groups.h>
+
 #include "capi.cuh"
 #include "common.cuh"
 
 namespace b200wd {
+namespace cg = cooperative_groups;
 
 constexpr int kMaxGrid = 148 * 4;
 constexpr int kBlock = 256;
@@ -25,21 +28,36 @@ __host__ __device__ __forceinline__ int64_t groups(int64_t n, int s) { return ((
 
 static inline int rows_per_block(int b) { return b >= kBlock ? 1 : kBlock / b; }
 
+// Reduction grid: at least kRowsPerThread (site, component) groups per thread
+// (small fields: fewer blocks, cheaper folds and grid barriers), at most
+// kMaxGrid blocks.  B200WD_RED_ROWS overrides (tuning).
+static inline int rows_per_thread() {
+  static int k = -1;
+  if (k < 0) {
+    const char* e = getenv("B200WD_RED_ROWS");
+    k = e ? atoi(e) : 4;
+    if (k < 1) k = 1;
+  }
+  return k;
+}
 static inline int grid_for_sites(int64_t n, int S) {
   n = ((n + 7) / 8) * 8 * 12;  // group count of a full spinor field (upper bound for s <= 12)
-  int64_t g = (n + S - 1) / S;
+  const int64_t per_block = (int64_t)S * rows_per_thread();
+  int64_t g = (n + per_block - 1) / per_block;
   if (g > kMaxGrid) g = kMaxGrid;
   return (int)(g < 1 ? 1 : g);
 }
 
 struct Scratch {
-  double2* partials;  // [kMaxGrid][b]
-  unsigned* ticket;
+  double2* partials;   // [kMaxGrid][b]
+  unsigned* ticket;    // 64 bytes
+  double2* partials2;  // [kMaxGrid][b], second buffer of the single-launch Arnoldi sweep
 };
 static inline Scratch scratch_of(void* p, int b) {
   Scratch s;
   s.partials = static_cast<double2*>(p);
   s.ticket = reinterpret_cast<unsigned*>(static_cast<char*>(p) + (size_t)kMaxGrid * b * sizeof(double2));
+  s.partials2 = reinterpret_cast<double2*>(reinterpret_cast<char*>(s.ticket) + 64);
   return s;
 }
 
@@ -269,10 +287,14 @@ __device__ void givens(double2 a, double2 bb, double& c, double2& s) {
   }
 }
 
-// close column j (gmres.py:135-157)
+// close column j (gmres.py:135-157), rhs r, from dot[r].x = ||w||^2
+__device__ void close_column_body(int j, const GState& g, int r);
 __global__ void close_column_kernel(int j, GState g) {
   const int r = threadIdx.x;
   if (r >= g.b) return;
+  close_column_body(j, g, r);
+}
+__device__ void close_column_body(int j, const GState& g, int r) {
   const int m = g.m;
   const double hn = sqrt(g.dot[r].x);
   const double en = g.eta_norm[r];
@@ -312,29 +334,36 @@ __global__ void close_column_kernel(int j, GState g) {
   g.relnorm[r] = en > 0 ? cabs_(gam[j + 1]) / fmax(en, kTiny) : 0.0;
 }
 
-// back substitution (gmres.py:161-177)
+// back substitution (gmres.py:161-177): one warp per rhs.  Row by row the lanes
+// form the products h[row][c] y[c] in parallel; lane 0 subtracts them in
+// ascending c, the same arithmetic and order as a sequential loop.
 __global__ void backsub_kernel(int jd, GState g) {
-  const int r = threadIdx.x;
+  __shared__ double2 ys[64], prod[64];
+  const int r = blockIdx.x, lane = threadIdx.x;
   if (r >= g.b) return;
   const int m = g.m;
   const double2* hh = g.h + (size_t)r * (m + 1) * m;
   const double2* gam = g.gamma + (size_t)r * (m + 1);
   double2* y = g.y + (size_t)r * m;
   for (int row = jd - 1; row >= 0; --row) {
-    double2 acc = gam[row];
-    for (int c2 = row + 1; c2 < jd; ++c2) {
-      const double2 t = cmul(hh[row * m + c2], y[c2]);
-      acc.x -= t.x;
-      acc.y -= t.y;
+    for (int c2 = row + 1 + lane; c2 < jd; c2 += 32) prod[c2] = cmul(hh[row * m + c2], ys[c2]);
+    __syncwarp();
+    if (lane == 0) {
+      double2 acc = gam[row];
+      for (int c2 = row + 1; c2 < jd; ++c2) {
+        acc.x -= prod[c2].x;
+        acc.y -= prod[c2].y;
+      }
+      const double2 dg = hh[row * m + row];
+      double2 yr = make_double2(0.0, 0.0);
+      if (cabs_(dg) > 0) {
+        const double den = dg.x * dg.x + dg.y * dg.y;
+        yr = make_double2((acc.x * dg.x + acc.y * dg.y) / den, (acc.y * dg.x - acc.x * dg.y) / den);
+      }
+      ys[row] = yr;
+      y[row] = yr;
     }
-    const double2 dg = hh[row * m + row];
-    if (cabs_(dg) > 0) {
-      // acc / dg
-      const double den = dg.x * dg.x + dg.y * dg.y;
-      y[row] = make_double2((acc.x * dg.x + acc.y * dg.y) / den, (acc.y * dg.x - acc.x * dg.y) / den);
-    } else {
-      y[row] = make_double2(0.0, 0.0);
-    }
+    __syncwarp();
   }
 }
 
@@ -345,23 +374,121 @@ struct ZList {
 
 // psi += sum_p y_p sigma_p Z_p  (one pass over psi and the basis)
 __global__ void update_kernel(int jd, int64_t n, int s, ZList zl, double2* __restrict__ psi, GState g) {
+  extern __shared__ double2 coef_s[];  // [jd][b]
   const int b = blockDim.x, r = threadIdx.x;
   const int m = g.m;
-  double2 coef[kMaxBasis];
-#pragma unroll 1
-  for (int p = 0; p < jd; ++p) {
+  for (int p = threadIdx.y; p < jd; p += blockDim.y) {
     const double2 yp = g.y[(size_t)r * m + p];
     const double sg = g.sigma[(size_t)p * g.b + r];
-    coef[p] = make_double2(yp.x * sg, yp.y * sg);
+    coef_s[p * b + r] = make_double2(yp.x * sg, yp.y * sg);
   }
+  __syncthreads();
+  const double2* coef = coef_s + r;
   const int64_t ng = groups(n, s);
   for (int64_t g = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; g < ng; g += (int64_t)gridDim.x * blockDim.y) {
       const int64_t i = g * b + r;
       double2 a = psi[i];
 #pragma unroll 1
-      for (int p = 0; p < jd; ++p) a = cmac(a, coef[p], __ldg(zl.z[p] + i));
+      for (int p = 0; p < jd; ++p) a = cmac(a, coef[p * b], __ldg(zl.z[p] + i));
       psi[i] = a;
     }
+}
+
+// ---- single-launch Arnoldi sweep (cooperative grid) --------------------------
+// The whole Gram-Schmidt sweep of column j -- <Z_0,w>, the j+1 fused MGS passes,
+// ||w||^2 and the column close -- in one launch with a grid barrier per
+// reduction instead of one kernel per pass.  Same grid, block shape, per-thread
+// site walk, block trees and partial fold order as gdot/mgs/reduce_finish, so
+// the results are bit-identical to the multi-launch sequence; every block folds
+// the partials itself (no ticket), partial buffers alternate between passes.
+__device__ __forceinline__ void block_partial(double2 v, double2* red, double2* out) {
+  const int b = blockDim.x, S = blockDim.y, r = threadIdx.x, y = threadIdx.y;
+  __syncthreads();  // red may still be read by the previous fold
+  red[y * b + r] = v;
+  __syncthreads();
+  int p2 = 1;
+  while (p2 < S) p2 <<= 1;
+  for (int stride = p2 >> 1; stride > 0; stride >>= 1) {
+    if (y < stride && y + stride < S) {
+      double2 a = red[y * b + r], c = red[(y + stride) * b + r];
+      red[y * b + r] = make_double2(a.x + c.x, a.y + c.y);
+    }
+    __syncthreads();
+  }
+  if (y == 0) out[(size_t)blockIdx.x * b + r] = red[r];
+}
+__device__ __forceinline__ double2 fold_partials(const double2* part, double2* red) {
+  const int b = blockDim.x, S = blockDim.y, r = threadIdx.x, y = threadIdx.y;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int q = y; q < (int)gridDim.x; q += S) {
+    double2 v = __ldcg(part + (size_t)q * b + r);
+    acc.x += v.x;
+    acc.y += v.y;
+  }
+  __syncthreads();
+  red[y * b + r] = acc;
+  __syncthreads();
+  int p2 = 1;
+  while (p2 < S) p2 <<= 1;
+  for (int stride = p2 >> 1; stride > 0; stride >>= 1) {
+    if (y < stride && y + stride < S) {
+      double2 a = red[y * b + r], c = red[(y + stride) * b + r];
+      red[y * b + r] = make_double2(a.x + c.x, a.y + c.y);
+    }
+    __syncthreads();
+  }
+  return red[r];
+}
+
+__global__ void arnoldi_sweep_kernel(int j, int64_t n, int s, ZList zl, double2* w, GState g) {
+  extern __shared__ double2 red[];
+  cg::grid_group grid = cg::this_grid();
+  const int b = blockDim.x, r = threadIdx.x, y = threadIdx.y;
+  const int m = g.m;
+  const int64_t ng = groups(n, s);
+  const int64_t g0 = (int64_t)blockIdx.x * blockDim.y + y, gst = (int64_t)gridDim.x * blockDim.y;
+  double2 a = make_double2(0.0, 0.0);
+  const double2* __restrict__ z0 = zl.z[0];
+  for (int64_t q = g0; q < ng; q += gst) {
+    const int64_t i = q * b + r;
+    acc_dot(a, __ldg(z0 + i), w[i]);
+  }
+  block_partial(a, red, g.sc.partials);
+  grid.sync();
+  double2 d = fold_partials(g.sc.partials, red);
+  for (int p = 0; p <= j; ++p) {
+    const double sig = g.sigma[(size_t)p * g.b + r];
+    const double2 hp = make_double2(sig * d.x, sig * d.y);
+    const double2 c = make_double2(-sig * hp.x, -sig * hp.y);
+    if (blockIdx.x == 0 && y == 0) g.h_raw[((size_t)r * (m + 1) + p) * m + j] = hp;
+    const double2* __restrict__ zp = zl.z[p];
+    a = make_double2(0.0, 0.0);
+    if (p < j) {
+      const double2* __restrict__ zn = zl.z[p + 1];
+      for (int64_t q = g0; q < ng; q += gst) {
+        const int64_t i = q * b + r;
+        const double2 wn = cmac(w[i], c, __ldg(zp + i));
+        w[i] = wn;
+        acc_dot(a, __ldg(zn + i), wn);
+      }
+    } else {
+      for (int64_t q = g0; q < ng; q += gst) {
+        const int64_t i = q * b + r;
+        const double2 wn = cmac(w[i], c, __ldg(zp + i));
+        w[i] = wn;
+        a.x = fma(wn.x, wn.x, a.x);
+        a.x = fma(wn.y, wn.y, a.x);
+      }
+    }
+    double2* buf = (p & 1) ? g.sc.partials : g.sc.partials2;
+    block_partial(a, red, buf);
+    grid.sync();
+    d = fold_partials(buf, red);
+  }
+  if (blockIdx.x == 0 && y == 0) {
+    g.dot[r] = d;
+    close_column_body(j, g, r);
+  }
 }
 
 static dim3 red_block(int b) { return dim3(b, rows_per_block(b)); }
@@ -372,7 +499,7 @@ static size_t red_smem(int b) { return (size_t)b * rows_per_block(b) * sizeof(do
 using namespace b200wd;
 
 extern "C" int64_t b200wd_reduce_scratch_bytes(int32_t b) {
-  return (int64_t)kMaxGrid * b * (int64_t)sizeof(double2) + 64;
+  return 2 * (int64_t)kMaxGrid * b * (int64_t)sizeof(double2) + 64;
 }
 
 #define CHECK_FIELD(n, s, b)                                                                        \
@@ -500,11 +627,55 @@ extern "C" int b200wd_gmres_update(const b200wd_gmres_state* st, int32_t j_done,
     B200WD_REQUIRE(z[p] != nullptr, "basis pointer %d is NULL", p);
     zl.z[p] = static_cast<const double2*>(z[p]);
   }
-  backsub_kernel<<<1, st->b, 0, as_stream(stream)>>>(j_done, gstate(st));
+  backsub_kernel<<<st->b, 32, 0, as_stream(stream)>>>(j_done, gstate(st));
   dim3 blk = red_block(st->b);
-  update_kernel<<<grid_for_sites(n_sites, blk.y), blk, 0, as_stream(stream)>>>(
+  update_kernel<<<grid_for_sites(n_sites, blk.y), blk, (size_t)j_done * st->b * sizeof(double2), as_stream(stream)>>>(
       j_done, n_sites, s, zl, static_cast<double2*>(psi), gstate(st));
   return check_launch("b200wd_gmres_update");
+}
+
+// Cooperative launch of arnoldi_sweep_kernel when the reduction grid is
+// co-resident (B200WD_NO_COOP=1 forces the per-pass launches).
+static bool sweep_single_launch(const b200wd_gmres_state* st, int j, int64_t n_sites, int s, const void* const* z,
+                                void* w, void* stream) {
+  static int en = -1;
+  if (en < 0) {
+    const char* e = getenv("B200WD_NO_COOP");
+    en = (e && e[0] == '1') ? 0 : 1;
+  }
+  if (!en) return false;
+  const dim3 blk = red_block(st->b);
+  const int grid = grid_for_sites(n_sites, blk.y);
+  const size_t smem = red_smem(st->b);
+  static int sm_count = 0, occ[kBlock + 1] = {0};
+  if (sm_count == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
+    int coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    if (!coop) en = 0;
+  }
+  if (!en) return false;
+  if (occ[st->b] == 0) {
+    int c = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, arnoldi_sweep_kernel, blk.x * blk.y, smem) != cudaSuccess)
+      c = -1;
+    occ[st->b] = c > 0 ? c : -1;
+  }
+  if (occ[st->b] < 0 || (int64_t)occ[st->b] * sm_count < grid) return false;
+  ZList zl{};
+  for (int p = 0; p <= j + 1; ++p) zl.z[p] = static_cast<const double2*>(z[p]);
+  GState g = gstate(st);
+  int jj = j, ss = s;
+  int64_t nn = n_sites;
+  double2* wp = static_cast<double2*>(w);
+  void* args[] = {&jj, &nn, &ss, &zl, &wp, &g};
+  if (cudaLaunchCooperativeKernel((const void*)arnoldi_sweep_kernel, dim3(grid), blk, args, smem,
+                                  as_stream(stream)) == cudaSuccess)
+    return true;
+  (void)cudaGetLastError();  // not sticky: fall back to the per-pass launches
+  return false;
 }
 
 extern "C" int b200wd_gmres_arnoldi(const b200wd_gmres_state* st, const b200wd_operator* op, int32_t j,
@@ -520,10 +691,14 @@ extern "C" int b200wd_gmres_arnoldi(const b200wd_gmres_state* st, const b200wd_o
   // w = A V_j = sigma_j A Z_j  (row j of sigma)
   const double* sig = static_cast<const double*>(st->sigma) + (int64_t)j * st->b;
   if (int rc = b200wd_operator_apply(op, st->b, z[j], w, sig, stream)) return rc;
-  if (int rc = b200wd_gmres_dot(st, n_sites, s, z[0], w, stream)) return rc;
-  for (int p = 0; p <= j; ++p)
-    if (int rc = b200wd_gmres_mgs(st, j, p, n_sites, s, w, z[p], p < j ? z[p + 1] : nullptr, stream)) return rc;
-  if (int rc = b200wd_gmres_close_column(st, j, stream)) return rc;
+  if (!sweep_single_launch(st, j, n_sites, s, z, w, stream)) {
+    if (int rc = b200wd_gmres_dot(st, n_sites, s, z[0], w, stream)) return rc;
+    for (int p = 0; p <= j; ++p)
+      if (int rc = b200wd_gmres_mgs(st, j, p, n_sites, s, w, z[p], p < j ? z[p + 1] : nullptr, stream)) return rc;
+    if (int rc = b200wd_gmres_close_column(st, j, stream)) return rc;
+  } else if (int rc = check_launch("b200wd_gmres_arnoldi (sweep)")) {
+    return rc;
+  }
   if (relnorm_host) {
     cudaStream_t cs = as_stream(stream);
     cudaError_t e = cudaMemcpyAsync(relnorm_host, st->relnorm, sizeof(double) * st->b, cudaMemcpyDeviceToHost, cs);

@@ -4,7 +4,7 @@ import torch
 import paper_2601_05816_b200 as P
 from paper_2601_05816_b200.device import upload
 from torch.profiler import profile, ProfilerActivity
-dims, b = (8, 4, 4, 4), 12
+dims, b = (8, 8, 8, 8), 4
 geom = P.LatticeGeometry(dims)
 gauge = P.flip_time_boundary(P.near_unit_gauge(geom, 0.3, 1))
 eta = upload(P.gen_spinor(geom.n_sites, b, 2, seed=2, geom=geom))
