@@ -880,6 +880,10 @@ __global__ void __launch_bounds__(256) halo_pack_kernel(const HopParams p, void*
   }
 }
 
+}  // namespace b200wd
+#include "tstream.cuh"
+namespace b200wd {
+
 static bool bulk_enabled() {
   static int en = -1;
   if (en < 0) {
@@ -892,6 +896,7 @@ static bool bulk_enabled() {
 template <typename R, int V, int B>
 static void launch_hop_b(const HopParams& p, cudaStream_t st) {
   if constexpr (B >= 4) {
+    if (bulk_enabled() && try_launch_tstream<R, V, B>(p, st)) return;
     if (bulk_enabled() && try_launch_ring<R, V, B>(p, st)) return;
   }
   const int bt = (B > 0 ? B : p.b) / V;

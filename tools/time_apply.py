@@ -1,0 +1,67 @@
+"""Time the D_W hop kernel on arbitrary lattices with device-generated fields.
+
+python tools/time_apply.py --dims 96 48 48 48 --b 12 --dtypes c128 c64 [--iters 10]
+
+Link and spinor VALUES are random numbers drawn on the device (not SU(3)):
+kernel time does not depend on them, and large lattices skip the host-side
+link generation.  Buffers rotate so > 4x L2 bytes are touched between reuses.
+Prints ms, site*rhs/s and the fraction of the measured HBM copy peak for the
+compulsory bytes (24 b + 36) w per site.
+"""
+import argparse
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2601_05816_b200 import _lib  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--dims", type=int, nargs=4, default=[32, 16, 16, 16])
+ap.add_argument("--b", type=int, nargs="+", default=[12])
+ap.add_argument("--dtypes", nargs="+", default=["c128", "c64"])
+ap.add_argument("--iters", type=int, default=10)
+a = ap.parse_args()
+pk = ROOT / "MEASURED_PEAKS.json"
+peak = float(json.loads(pk.read_text())["hbm_gbs"]) if pk.exists() else 6650.0
+T, X, Y, Z = a.dims
+n = T * X * Y * Z
+lat = _lib.Lattice.make(tuple(a.dims))
+l2 = 126 * 2**20
+for dt in a.dtypes:
+    tdt = torch.complex128 if dt == "c128" else torch.complex64
+    w = 16 if dt == "c128" else 8
+    code = 0 if dt == "c128" else 1
+    U = torch.randn((4 * (n // 8) * 72,), dtype=tdt, device="cuda")
+    for b in a.b:
+        fb = n * 12 * b * w
+        nbuf = max(1, int(np.ceil(4 * l2 / (2 * fb))))
+        ps = [torch.randn((n // 8, 12, 8, b), dtype=tdt, device="cuda") for _ in range(nbuf)]
+        es = [torch.empty_like(ps[0]) for _ in range(nbuf)]
+
+        def go(i):
+            x = ps[i % nbuf]
+            _lib.call("b200wd_hop", lat, code, b, -1, U.data_ptr(), x.data_ptr(), x.data_ptr(),
+                      es[i % nbuf].data_ptr(), 4.1, -1.0, None, 0, T, None, None, None)
+
+        for i in range(3):
+            go(i)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(a.iters):
+            go(i)
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / a.iters * 1e-3
+        alg = (24 * b + 36) * w * n
+        print(f"{dt} dims={a.dims} b={b:3d} {t*1e3:8.4f} ms  {n*b/t:10.3e} site*rhs/s  {alg/t/1e9:8.1f} GB/s  "
+              f"frac {alg/t/1e9/peak:.3f}", flush=True)
+        del ps, es
+        torch.cuda.empty_cache()
+    del U
