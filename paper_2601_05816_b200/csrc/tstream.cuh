@@ -191,6 +191,62 @@ __device__ __forceinline__ void ts_hop(cx<R> (&acc)[V][12], const cx<R>* sp, con
   ts_mv_acc<MU, FWD, R, V>(acc, up, h);
 }
 
+// L2 prefetch cursor over a CTA's concatenated (unit, slice) step sequence: the
+// own tile data of the step g.pf ahead is requested into L2 with
+// cp.async.bulk.prefetch, so the first-touch DRAM latency of a new column's
+// prologue / first steps overlaps the previous column's last steps.
+template <typename C, int NB, int LY, int B>
+struct TsPrefetch {
+  const HopParams& p;
+  const TsGrid& g;
+  const C* src;
+  const C* U;
+  int64_t u;
+  TsUnit w;
+  int s = 0;
+  __device__ TsPrefetch(const HopParams& p_, const TsGrid& g_, const C* s_, const C* u_)
+      : p(p_), g(g_), src(s_), U(u_), u(blockIdx.x) {
+    if (u < g.n_units) {
+      w = ts_decode(u, g);
+      s = w.t0 - 1;
+    }
+  }
+  __device__ void issue() const {
+    if (u >= g.n_units) return;
+    const int64_t nblk = p.n >> 3, line_blks = p.Z >> 3;
+    const int y = w.y * LY;
+    const int64_t bq = ts_blk(wrapi(s, p.T), w.x, y, w.zi, p, NB);
+    const int64_t bq1 = ts_blk(wrapi(s - 1, p.T), w.x, y, w.zi, p, NB);
+    const bool main = s >= w.t0 && s < w.t1;
+    for (int ll = 0; ll < LY; ++ll) {
+      const int64_t o = ll * line_blks;
+      bulk_prefetch_l2(src + (bq + o) * 96 * B, (uint32_t)(NB * 96 * B * sizeof(C)));
+      if (s >= w.t0) bulk_prefetch_l2(U + (bq1 + o) * 72, (uint32_t)(NB * 72 * sizeof(C)));
+      if (main) {
+#pragma unroll
+        for (int mu = 1; mu < 4; ++mu) bulk_prefetch_l2(U + (mu * nblk + bq + o) * 72, (uint32_t)(NB * 72 * sizeof(C)));
+      }
+    }
+  }
+  __device__ void advance() {
+    if (u >= g.n_units) return;
+    if (++s > w.t1) {
+      u += gridDim.x;
+      if (u < g.n_units) {
+        w = ts_decode(u, g);
+        s = w.t0 - 1;
+      }
+    }
+  }
+  __device__ void prime() {  // point the cursor g.pf steps ahead of the first step
+    for (int k = 0; k < g.pf; ++k) advance();
+  }
+  __device__ void step() {  // once per producer step
+    issue();
+    advance();
+  }
+};
+
 // ZG: segments are not whole z lines; the z hops at the segment edges read
 // global memory through generic pointers.
 template <typename R, int V, int B, int NB, int LY, bool ZG>
@@ -237,39 +293,15 @@ __global__ void __launch_bounds__(TsShape<R, V, B, NB, LY>::NT) hop_tstream_kern
         }
       };
       constexpr int SB = 96 * B;  // spinor complex per block
+      TsPrefetch<C, NB, LY, B> pfc(p, g, src, U);
+      if (g.pf > 0) pfc.prime();
       for (int64_t u = blockIdx.x; u < g.n_units; u += gridDim.x) {
         const TsUnit w = ts_decode(u, g);
         const int y = w.y * LY;
         for (int s = w.t0 - 1; s <= w.t1; ++s) {
           const int ts = wrapi(s, p.T);
           const int kind = s < w.t0 ? 0 : (s == w.t1 ? 2 : 1);  // prologue / main / epilogue
-          if (g.pf > 0) {  // warm L2 with the first-touch data of a later step of this column
-            const int sp = s + g.pf;
-            if (sp <= w.t1 && true) {
-              const int tp = wrapi(sp, p.T);
-              const int64_t bq = ts_blk(tp, w.x, y, w.zi, p, NB);
-              const int64_t bq1 = ts_blk(wrapi(sp - 1, p.T), w.x, y, w.zi, p, NB);
-              if (whole) {
-                bulk_prefetch_l2(src + bq * SB, (uint32_t)(Sh::SPIN * sizeof(C)));
-                bulk_prefetch_l2(U + (0 * nblk + bq1) * 72, (uint32_t)(Sh::LNK * sizeof(C)));
-                if (sp < w.t1) {
-#pragma unroll
-                  for (int mu = 1; mu < 4; ++mu)
-                    bulk_prefetch_l2(U + (mu * nblk + bq) * 72, (uint32_t)(Sh::LNK * sizeof(C)));
-                }
-              } else {
-                for (int ll = 0; ll < LY; ++ll) {
-                  bulk_prefetch_l2(src + (bq + ll * line_blks) * SB, (uint32_t)(Sh::SEGC * sizeof(C)));
-                  bulk_prefetch_l2(U + (0 * nblk + bq1 + ll * line_blks) * 72, (uint32_t)(Sh::LSEG * sizeof(C)));
-                  if (sp < w.t1) {
-#pragma unroll
-                    for (int mu = 1; mu < 4; ++mu)
-                      bulk_prefetch_l2(U + (mu * nblk + bq + ll * line_blks) * 72, (uint32_t)(Sh::LSEG * sizeof(C)));
-                  }
-                }
-              }
-            }
-          }
+          if (g.pf > 0) pfc.step();  // warm L2 with the own data g.pf steps ahead (across units)
           {  // own tile
             acquire();
             C* slot = ring + pslot * Sh::SLOT;

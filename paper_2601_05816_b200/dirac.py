@@ -159,7 +159,7 @@ class DiracOperator:
         hop_device(self.lat, self.dtype, v.b, -1, self.gauge, v, out, v, 4.0 + self.params.m0, -1.0, None,
                    t_begin, t_end, clover=self.clover, clover_mode=1, stream=stream)
 
-    def apply_host_pipelined(self, psi, out=None, chunks: int = 8):
+    def apply_host_pipelined(self, psi, out=None, chunks: int = 16):
         """Host field in -> host field out with the PCIe transfers overlapped.
 
         The lattice is cut into T-slab chunks.  Chunk c is copied H2D and
