@@ -321,7 +321,7 @@ __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, cons
       }
     }
     if (contiguous) {
-      if (H == 1)  // t-1 neighbour: the last use of these blocks in either order
+      if (H == 1 && p.hint_tm1)  // t-1 neighbour: the last use of these blocks in either order
         bulk_g2s_hint(slot, src + nb0 * 96 * B, Sh::SPIN * sizeof(C), full, pol_first);
       else if (H == 0 && p.hint_t1)  // t+1 neighbour: first touch
         bulk_g2s_hint(slot, src + nb0 * 96 * B, Sh::SPIN * sizeof(C), full, pol_t1);
@@ -582,6 +582,13 @@ static RingCfg ring_env() {
   return c;
 }
 
+// integer tuning knob from the environment (B200WD_L2HINT=0 turns the L2
+// eviction hints of the ring copies off; measured neutral on 48^3 x 96)
+static int ring_knob(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 // A T slice of the source field larger than this is not reused from L2 by
 // the t+1 hop of the next slice (tools/bench_strong.py on 48^3 x 96).
 constexpr int64_t kSliceNoReuse = 48ll << 20;
@@ -679,7 +686,9 @@ static bool launch_ring_nb(const HopParams& p_in, int64_t nblk, int S, cudaStrea
     // 10-25% slower than the natural order
     if (PAR) choose_tiles(p, Sh::F, NB, site_bytes);
     const int64_t slice_bytes = (int64_t)(p.per_t / Sh::F) * (int64_t)site_bytes;
-    p.hint_t1 = p.tile_x ? 2 : (slice_bytes > kSliceNoReuse ? 1 : 0);
+    const int hints = ring_knob("B200WD_L2HINT", 1);
+    p.hint_t1 = hints ? (p.tile_x ? 2 : (slice_bytes > kSliceNoReuse ? 1 : 0)) : 0;
+    p.hint_tm1 = hints;
     const bool whole_lines = (8 * Sh::F * NB) % p.Z == 0;
     if (S <= 0) S = (Sh::SLOT_BYTES >= 40 * 1024) ? (200 * 1024) / Sh::SLOT_BYTES : (100 * 1024) / Sh::SLOT_BYTES;
     if (S < 2) S = 2;

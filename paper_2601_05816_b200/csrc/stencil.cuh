@@ -49,6 +49,7 @@ struct HopParams {
   // slice exceeds L2: no reuse before eviction), 2 evict-last (patched order:
   // the blocks return as own blocks one patch slice later)
   int32_t hint_t1;
+  int32_t hint_tm1;  // 1: the t-1 neighbour tile (its last use) is copied evict-first
 };
 
 // y = M t for the two packed Hermitian 6x6 blocks of one site (fields.py:212-247:

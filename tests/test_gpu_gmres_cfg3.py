@@ -1,0 +1,42 @@
+"""BASELINE configs[3] GMRES parity against the reference run at (or near)
+full size: tests/golden/gmres_cfg3.json was produced by ``lqcdlab.solve_dirac``
+itself (tests/golden/make_golden_cfg3.py) on the inputs bench.py uses: near-unit
+links (eps=0.3, seed 3), antiperiodic T, Gaussian nrhs=12 rhs (seed 5), m0=0.1,
+GMRES(30), tol 1e-10, 67 restarts.  The GPU solve must take the same number of
+Arnoldi iterations (+-1), reach the tolerance on the full system, and follow the
+reference's per-iteration residual history to 1e-6 relative."""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+P = pytest.importorskip("paper_2601_05816_b200")
+GOLD = Path(__file__).resolve().parent / "golden" / "gmres_cfg3.json"
+
+
+def _gold(key):
+    if not GOLD.exists():
+        pytest.skip("gmres_cfg3.json not generated")
+    g = json.loads(GOLD.read_text())
+    if key not in g:
+        pytest.skip(f"{key} not in gmres_cfg3.json")
+    return g[key]
+
+
+@pytest.mark.parametrize("key", ["proxy_24x12c_full", "proxy_24x12c_oe", "cfg3_48x24c_oe"])
+def test_cfg3_solve_matches_reference(key):
+    from paper_2601_05816_b200.device import upload
+    g = _gold(key)
+    geom = P.LatticeGeometry(tuple(g["dims"]))
+    gauge = P.flip_time_boundary(P.near_unit_gauge(geom, g["eps"], g["link_seed"]))
+    eta = P.gen_spinor(geom.n_sites, g["b"], P.Layout.COMPONENT_MAJOR, seed=g["eta_seed"], geom=geom)
+    cfg = P.GmresConfig(restart_len=g["restart_len"], restarts=g["restarts"], tol=g["tol"])
+    rep = P.solve_dirac(P.DiracParams(m0=g["m0"]), gauge, None, upload(eta), cfg, odd_even=g["odd_even"])
+    assert abs(rep.iterations - g["iterations"]) <= 1, (rep.iterations, g["iterations"])
+    assert np.all(np.asarray(rep.full_relnorms) <= g["tol"])
+    ref_h = np.array(g["history"])
+    k = min(len(ref_h), len(rep.result.history))
+    got_h = np.array(rep.result.history[:k])
+    assert np.all(np.abs(got_h - ref_h[:k]) <= 1e-6 * ref_h[:k])

@@ -26,6 +26,7 @@ ap.add_argument("--dims", type=int, nargs=4, default=[32, 16, 16, 16])
 ap.add_argument("--b", type=int, nargs="+", default=[12])
 ap.add_argument("--dtypes", nargs="+", default=["c128", "c64"])
 ap.add_argument("--iters", type=int, default=10)
+ap.add_argument("--cold", action="store_true", help="time each launch alone after an L2 flush (512 MB memset)")
 a = ap.parse_args()
 pk = ROOT / "MEASURED_PEAKS.json"
 peak = float(json.loads(pk.read_text())["hbm_gbs"]) if pk.exists() else 6650.0
@@ -53,12 +54,25 @@ for dt in a.dtypes:
             go(i)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for i in range(a.iters):
-            go(i)
-        e1.record()
-        torch.cuda.synchronize()
-        t = e0.elapsed_time(e1) / a.iters * 1e-3
+        if a.cold:
+            flush = torch.empty(512 * 2**20, dtype=torch.uint8, device="cuda")
+            ts = []
+            for i in range(a.iters):
+                flush.fill_(i & 255)
+                e0.record()
+                go(i)
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e-3)
+            t = float(np.median(ts))
+            del flush
+        else:
+            e0.record()
+            for i in range(a.iters):
+                go(i)
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / a.iters * 1e-3
         alg = (24 * b + 36) * w * n
         print(f"{dt} dims={a.dims} b={b:3d} {t*1e3:8.4f} ms  {n*b/t:10.3e} site*rhs/s  {alg/t/1e9:8.1f} GB/s  "
               f"frac {alg/t/1e9/peak:.3f}", flush=True)
