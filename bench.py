@@ -220,6 +220,61 @@ def gpu_gmres(args, torch, P):
     return out
 
 
+def gmres_cpu_compare(torch, P, run_cpu: bool):
+    """GMRES time-to-solution on identical inputs, GPU vs host CPU.
+
+    * 24x12^3 (configs[3] physics: near-unit links seed 3, antiperiodic T,
+      nrhs=12 rhs seed 5, m0=0.1, GMRES(30), tol 1e-10): the GPU solve here
+      against lqcdlab itself, run on 1 core in the build container by
+      tests/golden/make_golden_cfg3.py (iterations and wall time from
+      tests/golden/gmres_cfg3.json; the reference cannot run on this box).
+    * 8^4 sample, same physics: the GPU solve against the oracle port timed
+      here on 1 host core (bounded: ~30 s)."""
+    from paper_2601_05816_b200.device import upload
+    gold_p = ROOT / "tests" / "golden" / "gmres_cfg3.json"
+    gold = json.loads(gold_p.read_text()) if gold_p.exists() else {}
+    cfg = P.GmresConfig(restart_len=30, restarts=67, tol=1e-10)
+    out = {}
+
+    def gpu_tts(dims, oe):
+        geom = P.LatticeGeometry(dims)
+        gauge = P.flip_time_boundary(P.near_unit_gauge(geom, 0.3, 3))
+        d_eta = upload(P.gen_spinor(geom.n_sites, 12, P.Layout.COMPONENT_MAJOR, seed=5, geom=geom))
+        P.solve_dirac(P.DiracParams(m0=M0), gauge, None, d_eta, P.GmresConfig(restart_len=2, restarts=1, tol=1e-10),
+                      odd_even=oe)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = P.solve_dirac(P.DiracParams(m0=M0), gauge, None, d_eta, cfg, odd_even=oe)
+        torch.cuda.synchronize()
+        return rep.iterations, time.perf_counter() - t0
+
+    for oe in (False, True):
+        key = f"proxy_24x12c_{'oe' if oe else 'full'}"
+        it, tts = gpu_tts((24, 12, 12, 12), oe)
+        rec = {"lattice": [24, 12, 12, 12], "gpu_iterations": it, "gpu_tts_s": tts}
+        if key in gold:
+            rec.update(reference_iterations=gold[key]["iterations"], reference_tts_s=gold[key]["reference_wall_s"],
+                       reference="lqcdlab 0.1.0 solve_dirac, 1 core, build container",
+                       speedup=gold[key]["reference_wall_s"] / tts)
+        out[key] = rec
+    it, tts = gpu_tts((8, 8, 8, 8), False)
+    rec = {"lattice": [8, 8, 8, 8], "gpu_iterations": it, "gpu_tts_s": tts}
+    if run_cpu:
+        from threadpoolctl import threadpool_limits
+
+        from oracle import lqcd_oracle as O
+        dims = (8, 8, 8, 8)
+        links = O.flip_time_boundary(O.near_unit_gauge(dims, 0.3, 3), dims)
+        eta = O.gen_spinor(4096, 12, 5)
+        with threadpool_limits(1):
+            t0 = time.perf_counter()
+            _, o, _ = O.solve_dirac(dims, M0, links, None, eta, O.GmresConfig(restart_len=30, restarts=67, tol=1e-10))
+            ct = time.perf_counter() - t0
+        rec.update(cpu_iterations=o.iterations, cpu_tts_s=ct, cpu_cores=1, cpu_kind="port", speedup=ct / tts)
+    out["sample_8c4_full"] = rec
+    return out
+
+
 def _slab_worker(args):
     """One T slab of the sample lattice (oracle restatement, halo.py semantics)."""
     from oracle import lqcd_oracle as O
@@ -392,6 +447,7 @@ def main():
     }
     if not args.no_gmres:
         line["gmres"] = gpu_gmres(args, torch, P)
+        line["gmres"]["cpu_compare"] = gmres_cpu_compare(torch, P, not args.no_cpu)
         sys.path.insert(0, str(ROOT / "tools"))
         from bench_schur import schur_bench
         line["schur"] = schur_bench()  # BASELINE configs[2]: 32^3x64 Schur apply, nrhs=12, c128
