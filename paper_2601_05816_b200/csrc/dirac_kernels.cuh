@@ -344,8 +344,11 @@ __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, cons
 
 // TILED: patched traversal order (checkerboard fields).  ZG: items are not
 // whole z lines, the z hops at the item edges read global memory.
+#ifndef B200WD_RING_MINB
+#define B200WD_RING_MINB 1  // experiment: CTAs per SM the register allocation must allow
+#endif
 template <typename R, int V, int B, int NB, bool PAR, bool TILED, bool ZG>
-__global__ void __launch_bounds__(RingShape<R, V, B, NB, PAR>::NT) hop_ring_kernel(const HopParams p,
+__global__ void __launch_bounds__(RingShape<R, V, B, NB, PAR>::NT, B200WD_RING_MINB) hop_ring_kernel(const HopParams p,
                                                                                    int64_t n_items, int S) {
   using C = cx<R>;
   using Sh = RingShape<R, V, B, NB, PAR>;
@@ -711,7 +714,6 @@ static bool launch_ring_nb(const HopParams& p_in, int64_t nblk, int S, cudaStrea
 // = defaults (whole z lines per item, ~100/200 KB ring).
 template <typename R, int V, int B>
 static RingCfg ring_table(int Z) {
-  (void)Z;
   if constexpr (sizeof(R) == 8) {
     switch (B) {
       case 4: return RingCfg{2, 3};
@@ -728,7 +730,7 @@ static RingCfg ring_table(int Z) {
       case 4: return RingCfg{4, 3};
       case 6: return RingCfg{4, 2};
       case 8: return RingCfg{2, 4};
-      case 12: return RingCfg{2, 2};
+      case 12: return Z >= 48 ? RingCfg{4, 3} : RingCfg{2, 2};  // 48^3x96: 0.381 vs 0.351
       case 16: return RingCfg{2, 2};
       case 24: return RingCfg{1, 3};
       case 32: return RingCfg{2, 4};

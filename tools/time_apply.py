@@ -26,6 +26,7 @@ ap.add_argument("--dims", type=int, nargs=4, default=[32, 16, 16, 16])
 ap.add_argument("--b", type=int, nargs="+", default=[12])
 ap.add_argument("--dtypes", nargs="+", default=["c128", "c64"])
 ap.add_argument("--iters", type=int, default=10)
+ap.add_argument("--parity", type=int, default=-1, help="destination parity of a checkerboard hop (-1: full)")
 ap.add_argument("--cold", action="store_true", help="time each launch alone after an L2 flush (512 MB memset)")
 a = ap.parse_args()
 pk = ROOT / "MEASURED_PEAKS.json"
@@ -40,14 +41,16 @@ for dt in a.dtypes:
     code = 0 if dt == "c128" else 1
     U = torch.randn((4 * (n // 8) * 72,), dtype=tdt, device="cuda")
     for b in a.b:
-        fb = n * 12 * b * w
+        nf = n if a.parity < 0 else n // 2
+        fb = nf * 12 * b * w
         nbuf = max(1, int(np.ceil(4 * l2 / (2 * fb))))
-        ps = [torch.randn((n // 8, 12, 8, b), dtype=tdt, device="cuda") for _ in range(nbuf)]
+        ps = [torch.randn((nf // 8, 12, 8, b), dtype=tdt, device="cuda") for _ in range(nbuf)]
         es = [torch.empty_like(ps[0]) for _ in range(nbuf)]
 
         def go(i):
             x = ps[i % nbuf]
-            _lib.call("b200wd_hop", lat, code, b, -1, U.data_ptr(), x.data_ptr(), x.data_ptr(),
+            _lib.call("b200wd_hop", lat, code, b, a.parity, U.data_ptr(), x.data_ptr(),
+                      x.data_ptr() if a.parity < 0 else None,
                       es[i % nbuf].data_ptr(), 4.1, -1.0, None, 0, T, None, None, None)
 
         for i in range(3):
@@ -73,8 +76,8 @@ for dt in a.dtypes:
             e1.record()
             torch.cuda.synchronize()
             t = e0.elapsed_time(e1) / a.iters * 1e-3
-        alg = (24 * b + 36) * w * n
-        print(f"{dt} dims={a.dims} b={b:3d} {t*1e3:8.4f} ms  {n*b/t:10.3e} site*rhs/s  {alg/t/1e9:8.1f} GB/s  "
+        alg = (24 * b + 36) * w * n if a.parity < 0 else (24 * b + 72) * w * nf  # parity: half fields, all links
+        print(f"{dt} dims={a.dims} par={a.parity} b={b:3d} {t*1e3:8.4f} ms  {nf*b/t:10.3e} site*rhs/s  {alg/t/1e9:8.1f} GB/s  "
               f"frac {alg/t/1e9/peak:.3f}", flush=True)
         del ps, es
         torch.cuda.empty_cache()
