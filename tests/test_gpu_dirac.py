@@ -306,10 +306,11 @@ def test_schur_ring_path_matches_oracle(dims, b, dtype, tol):
     assert rel(sp.reconstruct(red, el).ksi(), so.reconstruct(red_ref, el_ref)) < 1e-12
 
 
-@pytest.mark.parametrize("dims", [(4, 4, 4, 16), (4, 2, 6, 24), (4, 2, 2, 32)])
+@pytest.mark.parametrize("dims", [(4, 4, 4, 16), (4, 2, 6, 24), (4, 2, 2, 32), (4, 2, 2, 48)])
 @pytest.mark.parametrize("b", [4, 6, 12, 16, 24, 32])
 def test_ring_full_lattice_shapes(dims, b):
-    """Z = 16, 24, 32 exercise whole-line and partial-line (z-edge) ring items."""
+    """Z = 16, 24, 32, 48 exercise whole-line, partial-line (z-edge) and
+    line-straddling ring items (c64 nrhs 12 on Z >= 48 uses 32-site items)."""
     geom = P.LatticeGeometry(dims)
     links = O.near_unit_gauge(dims, 0.3, 23)
     psi = O.gen_spinor(geom.n_sites, b, 24)
