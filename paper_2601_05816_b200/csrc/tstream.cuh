@@ -250,7 +250,7 @@ struct TsPrefetch {
 // ZG: segments are not whole z lines; the z hops at the segment edges read
 // global memory through generic pointers.
 template <typename R, int V, int B, int NB, int LY, bool ZG>
-__global__ void __launch_bounds__(TsShape<R, V, B, NB, LY>::NT, B200WD_RING_MINB) hop_tstream_kernel(const HopParams p, const TsGrid g,
+__global__ void __launch_bounds__(TsShape<R, V, B, NB, LY>::NT) hop_tstream_kernel(const HopParams p, const TsGrid g,
                                                                                     int S) {
   using C = cx<R>;
   using Sh = TsShape<R, V, B, NB, LY>;
