@@ -344,11 +344,8 @@ __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, cons
 
 // TILED: patched traversal order (checkerboard fields).  ZG: items are not
 // whole z lines, the z hops at the item edges read global memory.
-#ifndef B200WD_RING_MINB
-#define B200WD_RING_MINB 1  // experiment: CTAs per SM the register allocation must allow
-#endif
 template <typename R, int V, int B, int NB, bool PAR, bool TILED, bool ZG>
-__global__ void __launch_bounds__(RingShape<R, V, B, NB, PAR>::NT, B200WD_RING_MINB) hop_ring_kernel(const HopParams p,
+__global__ void __launch_bounds__(RingShape<R, V, B, NB, PAR>::NT) hop_ring_kernel(const HopParams p,
                                                                                    int64_t n_items, int S) {
   using C = cx<R>;
   using Sh = RingShape<R, V, B, NB, PAR>;

@@ -44,6 +44,11 @@ template <typename R, int V, int B, int NB, int LY> struct TsShape {
   static constexpr int NC = BT * SEG * LY;      // consumer threads
   static constexpr int NCW = NC / 32;           // consumer warps
   static constexpr int NT = NC + 32;            // + producer warp
+  // CTAs per SM the register allocation must allow.  With 5 (or 3) warps per
+  // CTA some SM sub-partitions hold one warp more than others, so two CTAs fit
+  // only if ptxas keeps 3 warps within the 16K registers of a sub-partition
+  // (<= 168 per thread); otherwise a 160-thread CTA runs alone on its SM.
+  static constexpr int MINB = NT <= 96 ? 4 : (NT <= 160 ? 2 : 1);
   static constexpr int SEGC = NB * 96 * B;      // spinor complex per segment
   static constexpr int LSEG = NB * 72;          // link complex per segment, one direction
   static constexpr int SPIN = LY * SEGC;        // own / x tiles: LY segments
@@ -250,7 +255,7 @@ struct TsPrefetch {
 // ZG: segments are not whole z lines; the z hops at the segment edges read
 // global memory through generic pointers.
 template <typename R, int V, int B, int NB, int LY, bool ZG>
-__global__ void __launch_bounds__(TsShape<R, V, B, NB, LY>::NT) hop_tstream_kernel(const HopParams p, const TsGrid g,
+__global__ void __launch_bounds__(TsShape<R, V, B, NB, LY>::NT, TsShape<R, V, B, NB, LY>::MINB) hop_tstream_kernel(const HopParams p, const TsGrid g,
                                                                                     int S) {
   using C = cx<R>;
   using Sh = TsShape<R, V, B, NB, LY>;
