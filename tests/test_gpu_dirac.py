@@ -341,3 +341,37 @@ def test_host_pipelined_apply_matches_device_apply(layout):
         op = P.DiracOperator(P.DiracParams(m0=0.1), P.GaugeField(geom, links), None)
         op.apply_host_pipelined(f, o, chunks=chunks)
         assert rel(o.ksi(), ref) < 1e-12
+
+
+@pytest.mark.parametrize("dims", [(2, 2, 2, 2), (2, 4, 2, 6), (6, 2, 2, 4)])
+@pytest.mark.parametrize("b", [5, 7, 10, 40])
+def test_runtime_nrhs_and_small_lattices(dims, b):
+    """nrhs outside the compiled set (the runtime-b kernel), the minimum 2^4
+    lattice and z extents 2/4/6 (generic kernel), full operator and Schur, c128
+    and c64."""
+    geom = P.LatticeGeometry(dims)
+    links = O.flip_time_boundary(O.near_unit_gauge(dims, 0.3, 31 + b), dims)
+    psi = O.gen_spinor(geom.n_sites, b, 32 + b)
+    gauge = P.GaugeField(geom, links)
+    ref = O.apply_dirac(dims, 0.1, links, None, psi)
+    got = P.apply_dirac(P.DiracParams(m0=0.1), gauge, None, host_field(psi, 2, geom))
+    assert rel(got.ksi(), ref) < 1e-12
+    got64 = P.apply_dirac(P.DiracParams(m0=0.1), gauge, None, host_field(psi, 1, geom), dtype="c64")
+    assert rel(got64.ksi(), O.apply_dirac(dims, 0.1, O.round_c64(links), None, O.round_c64(psi))) < 1e-5
+    v = O.gen_spinor(geom.n_sites // 2, b, 33 + b)
+    so = O.SchurOracle(dims, 0.1, links, None, keep_parity=0)
+    sp = P.SchurOperator(P.DiracParams(m0=0.1), gauge, None, keep_parity=0)
+    assert rel(sp.apply(host_field(v, 2)).ksi(), so.apply(v)) < 1e-12
+
+
+def test_max_nrhs():
+    """b = 128, the largest rhs block the ABI accepts; 129 is rejected."""
+    dims = (2, 2, 2, 4)
+    geom = P.LatticeGeometry(dims)
+    links = O.gen_gauge_random(dims, 5)
+    psi = O.gen_spinor(geom.n_sites, 128, 6)
+    got = P.apply_dirac(P.DiracParams(m0=0.1), P.GaugeField(geom, links), None, host_field(psi, 2, geom))
+    assert rel(got.ksi(), O.apply_dirac(dims, 0.1, links, None, psi)) < 1e-12
+    with pytest.raises(ValueError):
+        P.apply_dirac(P.DiracParams(m0=0.1), P.GaugeField(geom, links), None,
+                      host_field(O.gen_spinor(geom.n_sites, 129, 6), 2, geom))
