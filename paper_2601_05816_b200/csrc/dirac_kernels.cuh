@@ -344,8 +344,13 @@ __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, cons
 
 // TILED: patched traversal order (checkerboard fields).  ZG: items are not
 // whole z lines, the z hops at the item edges read global memory.
+#ifdef B200WD_RING_MINB  // experiment builds only: CTAs per SM the register allocation must allow
+#define B200WD_RING_BOUNDS(...) __launch_bounds__(__VA_ARGS__, B200WD_RING_MINB)
+#else
+#define B200WD_RING_BOUNDS(...) __launch_bounds__(__VA_ARGS__)
+#endif
 template <typename R, int V, int B, int NB, bool PAR, bool TILED, bool ZG>
-__global__ void __launch_bounds__(RingShape<R, V, B, NB, PAR>::NT) hop_ring_kernel(const HopParams p,
+__global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_kernel(const HopParams p,
                                                                                    int64_t n_items, int S) {
   using C = cx<R>;
   using Sh = RingShape<R, V, B, NB, PAR>;
