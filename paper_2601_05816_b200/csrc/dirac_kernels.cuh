@@ -691,7 +691,7 @@ static bool launch_ring_nb(const HopParams& p_in, int64_t nblk, int S, cudaStrea
     // 10-25% slower than the natural order
     if (PAR) choose_tiles(p, Sh::F, NB, site_bytes);
     const int64_t slice_bytes = (int64_t)(p.per_t / Sh::F) * (int64_t)site_bytes;
-    const int hints = ring_knob("B200WD_L2HINT", 1);
+    static const int hints = ring_knob("B200WD_L2HINT", 1);  // read once per process
     p.hint_t1 = hints ? (p.tile_x ? 2 : (slice_bytes > kSliceNoReuse ? 1 : 0)) : 0;
     p.hint_tm1 = hints;
     const bool whole_lines = (8 * Sh::F * NB) % p.Z == 0;
