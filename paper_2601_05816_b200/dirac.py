@@ -162,13 +162,14 @@ class DiracOperator:
     def apply_host_pipelined(self, psi, out=None, chunks: int = 16):
         """Host field in -> host field out with the PCIe transfers overlapped.
 
-        The lattice is cut into T-slab chunks.  Chunk c is copied H2D and
-        converted to the device layout on an upload stream; as soon as chunk
-        c+1 has landed, the D slices of chunk c are computed (their t+1
-        neighbours are now resident), converted back and copied D2H on a
-        download stream, so uploads, compute and downloads of different chunks
-        overlap (PCIe is full duplex).  Chunk 0 waits for the last chunk (the
-        periodic T wrap).  Results are identical to the unpipelined apply.
+        The lattice is cut into T-slab chunks, copied H2D and converted to
+        the device layout on an upload stream, the last chunk first (it holds
+        slice 0's t-1 neighbour).  As chunk c lands, the slices
+        [c*tc - 1, (c+1)*tc - 1) have both T neighbours resident; they are
+        computed, converted back and copied D2H on a download stream at once,
+        so uploads, compute and downloads overlap (PCIe is full duplex) and only
+        tc + 1 slices remain after the last upload.  Results are identical to
+        the unpipelined apply.
         """
         import torch
 
@@ -195,25 +196,30 @@ class DiracOperator:
         s_up.wait_stream(cur)
         chunk = tc * per_t * s * b  # complex elements per chunk (both layouts are site-major)
         esz = d_psi.data.element_size()
-        up_ev = []
+        up_order = [nck - 1] + list(range(nck - 1))  # the last chunk first: slice 0's t-1 neighbour
+        up_ev = {}
         with torch.cuda.stream(s_up):
-            for c in range(nck):
+            for c in up_order:
                 sl = slice(c * chunk, (c + 1) * chunk)
                 raw_in[sl].copy_(host_in[sl], non_blocking=True)
                 _lib.call("b200wd_spinor_import", raw_in[sl].data_ptr(), layout, tc * per_t, s, b,
                           d_psi.ptr + c * chunk * esz, dtype_code(self.dtype), stream_ptr(s_up))
                 ev = torch.cuda.Event()
                 ev.record(s_up)
-                up_ev.append(ev)
-        order = list(range(1, nck)) + [0]
-        for c in order:
-            cur.wait_event(up_ev[(c + 1) % nck])
-            if c == 0:
-                cur.wait_event(up_ev[0])
-            self.apply_range(d_psi, d_eta, c * tc, (c + 1) * tc, cur)
-            sl = slice(c * chunk, (c + 1) * chunk)
-            _lib.call("b200wd_spinor_export", d_eta.ptr + c * chunk * esz, dtype_code(self.dtype), tc * per_t, s,
-                      b, raw_out[sl].data_ptr(), layout, stream_ptr(cur))
+                up_ev[c] = ev
+        # As chunk c lands, the slices [c*tc - 1, (c+1)*tc - 1) have both T
+        # neighbours resident: compute them and send them back at once.
+        ranges = [(0, tc - 1, 0)] + [(c * tc - 1, (c + 1) * tc - 1, c) for c in range(1, nck - 1)]
+        ranges.append(((nck - 1) * tc - 1, T, up_order[-1]))
+        per_slice = per_t * s * b
+        for t0, t1, c in ranges:
+            if t1 <= t0:
+                continue
+            cur.wait_event(up_ev[c])
+            self.apply_range(d_psi, d_eta, t0, t1, cur)
+            sl = slice(t0 * per_slice, t1 * per_slice)
+            _lib.call("b200wd_spinor_export", d_eta.ptr + t0 * per_slice * esz, dtype_code(self.dtype),
+                      (t1 - t0) * per_t, s, b, raw_out[sl].data_ptr(), layout, stream_ptr(cur))
             s_dn.wait_stream(cur)
             with torch.cuda.stream(s_dn):
                 host_out[sl].copy_(raw_out[sl], non_blocking=True)

@@ -341,6 +341,11 @@ def test_host_pipelined_apply_matches_device_apply(layout):
         op = P.DiracOperator(P.DiracParams(m0=0.1), P.GaugeField(geom, links), None)
         op.apply_host_pipelined(f, o, chunks=chunks)
         assert rel(o.ksi(), ref) < 1e-12
+    ref64 = O.apply_dirac(dims, 0.1, O.round_c64(links), None, O.round_c64(psi))
+    for chunks in (3, 16):  # 16 % 3 != 0: falls back to 2 chunks
+        op = P.DiracOperator(P.DiracParams(m0=0.1), P.GaugeField(geom, links), None, "c64")
+        op.apply_host_pipelined(f, o, chunks=chunks)
+        assert rel(o.ksi(), ref64) < 1e-5
 
 
 @pytest.mark.parametrize("dims", [(2, 2, 2, 2), (2, 4, 2, 6), (6, 2, 2, 4)])
