@@ -226,6 +226,14 @@ def gpu_gmres(args, torch, P):
         out["oe" if oe else "full"] = {"iterations": rep.iterations, "time_to_solution_s": tts,
                                        "s_per_iteration": tts / max(rep.iterations, 1),
                                        "max_full_relnorm": float(rep.full_relnorms.max())}
+        gold_p = ROOT / "tests" / "golden" / "gmres_cfg3.json"
+        gold = json.loads(gold_p.read_text()) if gold_p.exists() else {}
+        if oe and "cfg3_48x24c_oe" in gold:  # lqcdlab itself on these inputs, 1 core, build container
+            g = gold["cfg3_48x24c_oe"]
+            out["oe"].update(reference_iterations=g["iterations"], reference_tts_s=g["reference_wall_s"],
+                             reference_max_full_relnorm=max(g["full_relnorms"]),
+                             reference="lqcdlab 0.1.0 solve_dirac(odd_even=True), 1 core, build container",
+                             speedup_vs_reference=g["reference_wall_s"] / tts)
     return out
 
 
