@@ -2,7 +2,7 @@
 
 Run in the build container only (needs /root/reference); long-running:
 
-    PYTHONPATH=/root/reference/pkg/src nice python tests/golden/make_golden_cfg3.py [proxy|oe|all]
+    PYTHONPATH=/root/reference/pkg/src nice python tests/golden/make_golden_cfg3.py [proxy|oe|mid|all]
 
 configs[3]: batched restarted GMRES(30), nrhs=12 Gaussian rhs, m0=0.1,
 near-unit links (eps=0.3), antiperiodic T, C=0, relative tolerance 1e-10,
@@ -16,6 +16,7 @@ the package's) and fed to ``lqcdlab.solve_dirac`` unchanged.
 * ``oe``: the full-size 48 x 24^3 odd-even solve (about 1.3 h on one core,
   ~40 GB; the full-size unpreconditioned solve needs ~58 GB of host memory
   for its 31-vector basis and is not run here).
+* ``mid``: the unpreconditioned solve on 32 x 16^3 (~20 min, ~10 GB).
 
 Writes tests/golden/gmres_cfg3.json (iterations, per-iteration relnorm
 history, final and full-system residuals, wall time of the reference).
@@ -71,6 +72,8 @@ def main():
             save(f"proxy_24x12c_{'oe' if oe else 'full'}", run((24, 12, 12, 12), oe))
     if what in ("oe", "all"):
         save("cfg3_48x24c_oe", run((48, 24, 24, 24), True))
+    if what in ("mid", "all"):
+        save("mid_32x16c_full", run((32, 16, 16, 16), False))
 
 
 if __name__ == "__main__":

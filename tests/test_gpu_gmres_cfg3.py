@@ -25,7 +25,7 @@ def _gold(key):
     return g[key]
 
 
-@pytest.mark.parametrize("key", ["proxy_24x12c_full", "proxy_24x12c_oe", "cfg3_48x24c_oe"])
+@pytest.mark.parametrize("key", ["proxy_24x12c_full", "proxy_24x12c_oe", "mid_32x16c_full", "cfg3_48x24c_oe"])
 def test_cfg3_solve_matches_reference(key):
     from paper_2601_05816_b200.device import upload
     g = _gold(key)
