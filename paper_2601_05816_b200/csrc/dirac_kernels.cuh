@@ -895,6 +895,7 @@ __global__ void __launch_bounds__(256) halo_pack_kernel(const HopParams p, void*
 
 }  // namespace b200wd
 #include "tstream.cuh"
+#include "ring2.cuh"
 namespace b200wd {
 
 static bool bulk_enabled() {
@@ -910,6 +911,7 @@ template <typename R, int V, int B>
 static void launch_hop_b(const HopParams& p, cudaStream_t st) {
   if constexpr (B >= 4) {
     if (bulk_enabled() && try_launch_tstream<R, V, B>(p, st)) return;
+    if (bulk_enabled() && try_launch_ring2<R, V, B>(p, st)) return;
     if (bulk_enabled() && try_launch_ring<R, V, B>(p, st)) return;
   }
   const int bt = (B > 0 ? B : p.b) / V;

@@ -660,7 +660,8 @@ static bool launch_ts_nb(const HopParams& p, int S, int nch, int pf, int px, int
 
 // Where the stream is used by default: (NB, LY, S) per (dtype, b), measured on
 // B200 against the ring kernel (tools/tune_ts.sh, tools/time_apply.py; DESIGN
-// section 3): c64 b=8 0.072 vs 0.078 ms, c64 b=16 0.124 vs 0.130 ms on 16^3x32.
+// section 3): c64 b=16 0.124 vs 0.130 ms on 16^3x32 (c64 b=8: 0.072 vs 0.078,
+// superseded by the two-line ring at 0.070).
 // Everywhere else the ring kernel measured equal or faster (c128: the stream's
 // consumers are bound by FP64 / shared-memory latency at 8 warps per SM while
 // the ring is bound by L2 -> SM bytes at a similar time), so nb = 0 disables.
@@ -668,8 +669,7 @@ static bool launch_ts_nb(const HopParams& p, int S, int nch, int pf, int px, int
 template <typename R, int V, int B>
 static TsCfg ts_table() {
   if constexpr (sizeof(R) == 4) {
-    if (B == 8) return TsCfg{2, 1, 2, 0};
-    if (B == 16) return TsCfg{2, 1, 4, 0};
+    if (B == 16) return TsCfg{2, 1, 4, 0};  // (c64 nrhs 8: the two-line ring, ring2.cuh, measured faster)
   }
   return TsCfg{};
 }

@@ -1,4 +1,4 @@
-"""Run in a subprocess with B200WD_TS_CFG set (read once per process): the
+"""Run in a subprocess with B200WD_TS_CFG or B200WD_RING2_S set (read once per process): the
 T-streaming hop kernel in a forced shape vs the oracle, on lattices that
 exercise whole-line and partial-line (z-edge) segments, one and several t
 chunks, patched column order and a slice sub-range (the T-split interior
