@@ -721,7 +721,7 @@ static RingCfg ring_table(int Z) {
       case 4: return RingCfg{2, 3};
       case 6: return RingCfg{2, 3};
       case 8: return RingCfg{2, 4};
-      case 12: return RingCfg{2, 4};
+      case 12: return RingCfg{2, 5};  // 16^3x32: 0.556 vs 0.523 at S=4
       case 16: return RingCfg{2, 4};
       case 24: return RingCfg{1, 6};
       case 32: return RingCfg{2, 6};
@@ -795,6 +795,8 @@ static bool try_launch_ring(const HopParams& p, cudaStream_t st) {
     RingCfg cp{};
     if constexpr (sizeof(R) == 8) {
       if (B == 4 || B == 8) cp = RingCfg{2, 3};
+      if (B == 12) cp = RingCfg{2, 5};  // 32^3x64 parity hop: 0.573 vs 0.541 (default depth)
+      if (B == 16) cp = RingCfg{2, 4};  // 0.546 vs 0.517
     } else {
       if (B == 8) cp = RingCfg{2, 3};
     }
