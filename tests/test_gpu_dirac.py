@@ -281,9 +281,9 @@ def test_gmres_clover_matches_reference_golden():
     assert np.abs(d.psi.ksi() - s.psi.ksi()).max() / np.abs(d.psi.ksi()).max() < 1e-7
 
 
-@pytest.mark.parametrize("dims", [(4, 4, 4, 16), (4, 2, 2, 32), (6, 2, 4, 16)])
-@pytest.mark.parametrize("b,dtype,tol", [(4, "c128", 1e-12), (12, "c128", 1e-12), (8, "c64", 1e-5),
-                                         (16, "c64", 1e-5)])
+@pytest.mark.parametrize("dims", [(4, 4, 4, 16), (4, 2, 2, 32), (6, 2, 4, 16), (4, 2, 2, 48)])
+@pytest.mark.parametrize("b,dtype,tol", [(4, "c128", 1e-12), (12, "c128", 1e-12), (16, "c128", 1e-12),
+                                         (8, "c64", 1e-5), (16, "c64", 1e-5)])
 def test_schur_ring_path_matches_oracle(dims, b, dtype, tol):
     """Z % 16 == 0 lattices take the checkerboard TMA ring kernel."""
     geom = P.LatticeGeometry(dims)
