@@ -795,8 +795,9 @@ static bool try_launch_ring(const HopParams& p, cudaStream_t st) {
     RingCfg cp{};
     if constexpr (sizeof(R) == 8) {
       if (B == 4 || B == 8) cp = RingCfg{2, 3};
-      if (B == 12) cp = RingCfg{2, 5};  // 32^3x64 parity hop: 0.573 vs 0.541 (default depth)
-      if (B == 16) cp = RingCfg{2, 4};  // 0.546 vs 0.517
+      // nrhs 12 / 16 keep the default depth: deeper rings are faster for a lone
+      // hop without xself (0.573 vs 0.541, 0.546 vs 0.517) but slower for the
+      // Schur apply, whose second hop reads xself (4.20 vs 4.03 ms, 5.60 vs 5.32 ms)
     } else {
       if (B == 8) cp = RingCfg{2, 3};
     }
