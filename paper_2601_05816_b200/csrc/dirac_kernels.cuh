@@ -34,7 +34,10 @@ namespace b200wd {
 
 // Threads per block of the hopping kernel and the occupancy target handed
 // to ptxas (c128: <= 168 registers -> 3 blocks = 12 warps per SM; c64: 4 blocks).
-constexpr int kHopThreads = 128;
+#ifndef B200WD_HOP_THREADS
+#define B200WD_HOP_THREADS 128
+#endif
+constexpr int kHopThreads = B200WD_HOP_THREADS;
 #ifndef B200WD_MINB_C128
 #define B200WD_MINB_C128 3
 #endif
