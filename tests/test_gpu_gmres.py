@@ -249,3 +249,21 @@ def test_operator_apply_matches_apply_device():
     bad = _lib.Operator()
     with pytest.raises(ValueError):
         _lib.call("b200wd_operator_apply", ctypes.byref(bad), 6, v.ptr, out.ptr, None, stream_ptr())
+
+
+@pytest.mark.parametrize("b,oe", [(1, False), (5, True), (7, False)])
+def test_gmres_runtime_nrhs_matches_oracle(b, oe):
+    """Batched GMRES with nrhs outside the compiled set (runtime-b kernels)."""
+    dims = (4, 4, 4, 4)
+    geom = P.LatticeGeometry(dims)
+    links = O.flip_time_boundary(O.near_unit_gauge(dims, 0.3, 51), dims)
+    eta = O.gen_spinor(geom.n_sites, b, 52)
+    cfg = P.GmresConfig(restart_len=12, restarts=20, tol=1e-10)
+    f = P.BlockSpinorField.zeros(geom.n_sites, b, P.Layout.COMPONENT_MAJOR, geom=geom)
+    f.set_ksi(eta)
+    rep = P.solve_dirac(P.DiracParams(m0=0.1), P.GaugeField(geom, links), None, f, cfg, odd_even=oe)
+    psi, out, _ = O.solve_dirac(dims, 0.1, links, None, eta,
+                                O.GmresConfig(restart_len=12, restarts=20, tol=1e-10), odd_even=oe)
+    assert abs(rep.iterations - out.iterations) <= 1
+    assert np.all(rep.full_relnorms <= 1e-10)
+    assert np.abs(rep.psi.ksi() - psi).max() / np.abs(psi).max() < 1e-8
