@@ -220,11 +220,12 @@ __global__ void __launch_bounds__(Ring2Shape<R, V, B, NB>::NT) hop_ring2_kernel(
 // > 1 forces that ring depth).
 // Measured on 16^3x32 (profiles/r1_tstream_tuning.txt, ring2 section): c64
 // nrhs 4 0.0434 vs 0.0460 ms (ring), nrhs 8 0.0701 vs 0.0727 ms (stream);
-// c128 nrhs 4/8 and c64 nrhs 16 were slower or equal.
+// c128 nrhs 4/8 and c64 nrhs 12/16/24 were slower or equal.
 template <typename R, int V, int B>
 static int ring2_table() {
   if constexpr (sizeof(R) == 4) {
     if (B == 4) return 3;
+    if (B == 6) return 3;  // 0.0620 vs 0.0682 ms (ring)
     if (B == 8) return 2;
   }
   return 0;
