@@ -29,6 +29,9 @@ _LAZY = {
     "DeviceField": "device", "DeviceGauge": "device", "upload": "device", "download": "device",
     "upload_gauge": "device",
     "TSplitComm": "tsplit",
+    "MultiRankExecutor": "multirank", "apply_dirac_multirank": "multirank", "EpochStats": "multirank",
+    "arithmetic_intensity": "perf", "theoretical_perf": "perf", "read_write_ratio": "perf",
+    "effective_bandwidth": "perf", "arch_efficiency": "perf", "CounterSample": "perf",
 }
 
 

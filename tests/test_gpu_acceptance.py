@@ -112,3 +112,22 @@ def test_reduce_dense_solve_reconstruct_and_wrappers(lattice44):
     x_odd = P.reconstruct_full(prm, u, c, x, elim)
     assert np.abs(x_odd.ksi() - s.reconstruct(x, elim).ksi()).max() == 0.0
     assert dense.n_sites == s.n_sites
+
+
+@pytest.mark.parametrize("ranks", [1, 2, 4])
+@pytest.mark.parametrize("with_clover", [False, True])
+def test_multirank_executor_matches_single_rank(ranks, with_clover):
+    """apply_dirac(..., comm=MultiRankExecutor(grid)) (halo.py:216-401): rank
+    slabs with device halo exchange reproduce the single-rank apply."""
+    dims = (8, 4, 4, 8)
+    geom = P.LatticeGeometry(dims)
+    gauge = P.gen_gauge(geom, "random", seed=61)
+    clover = P.gen_clover(geom, "random", scale=0.1, seed=62) if with_clover else P.gen_clover(geom, "zero")
+    psi = P.gen_spinor(geom.n_sites, 4, P.Layout.COMPONENT_MAJOR, seed=63, geom=geom)
+    params = P.DiracParams(m0=0.1)
+    ref = P.apply_dirac(params, gauge, clover, psi).ksi()
+    got, ex = P.apply_dirac_multirank(params, gauge, clover, psi, P.RankGrid((ranks, 1, 1, 1)))
+    assert np.linalg.norm(got.ksi() - ref) / np.linalg.norm(ref) < 1e-14
+    assert len(ex.last_stats) == ranks
+    via_comm = P.apply_dirac(params, gauge, clover, psi, comm=P.MultiRankExecutor(P.RankGrid((ranks, 1, 1, 1))))
+    assert np.array_equal(via_comm.ksi(), got.ksi())

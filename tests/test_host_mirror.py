@@ -131,3 +131,27 @@ def test_near_unit_links_forked_workers_same_bits():
     ref = near_unit_links(dims, 0.3, 5)
     assert np.array_equal(near_unit_links(dims, 0.3, 5, workers=4), ref)
     assert np.array_equal(near_unit_links(dims, 0.3, 5, 1, 5, workers=3), ref[32:160])
+
+
+def test_multirank_executor_arguments():
+    """halo.py:225-233 argument rules; the B200 executor splits T only."""
+    P.MultiRankExecutor(P.RankGrid((2, 1, 1, 1)), mode="threads")
+    with pytest.raises(ValueError):
+        P.MultiRankExecutor(P.RankGrid((2, 1, 1, 1)), mode="processes")
+    with pytest.raises(NotImplementedError):
+        P.MultiRankExecutor(P.RankGrid((1, 2, 1, 1)))
+
+
+def test_perf_model_formulas():
+    """perf.py:64-99: AI(1) = 0.570, AI(16) = 0.919 (PAPER.md:171-176), ratios, bandwidth."""
+    from fractions import Fraction
+    assert abs(float(P.arithmetic_intensity(1)) - 0.570) < 1e-3
+    assert abs(float(P.arithmetic_intensity(16)) - 0.919) < 1e-3
+    assert P.read_write_ratio(2) == Fraction(204 * 2 + 330, 408)
+    assert P.theoretical_perf(1e9, 4) == 1e9 * float(P.arithmetic_intensity(4))
+    s = P.CounterSample(l2_refill=100, l2_writeback=50, cycles=1000, frequency=2e9, ranks=2)
+    assert P.effective_bandwidth(s) == 150 * 256 * 2e9 / 1000 * 2
+    with pytest.raises(ValueError):
+        P.arithmetic_intensity(0)
+    with pytest.raises(ValueError):
+        P.CounterSample(-1, 0, 1, 1.0)
