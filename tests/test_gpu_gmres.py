@@ -267,3 +267,29 @@ def test_gmres_runtime_nrhs_matches_oracle(b, oe):
     assert abs(rep.iterations - out.iterations) <= 1
     assert np.all(rep.full_relnorms <= 1e-10)
     assert np.abs(rep.psi.ksi() - psi).max() / np.abs(psi).max() < 1e-8
+
+
+def test_solve_layouts_and_foreign_fields_agree():
+    """The same solve from Layout 1 and Layout 2 host fields, and from a
+    duck-typed foreign field object (the way lqcdlab's own dataclasses are
+    accepted: n_sites, s, b, layout, data), gives identical results."""
+    from types import SimpleNamespace
+    dims = (4, 4, 4, 8)
+    geom = P.LatticeGeometry(dims)
+    links = O.flip_time_boundary(O.near_unit_gauge(dims, 0.3, 71), dims)
+    eta = O.gen_spinor(geom.n_sites, 6, 72)
+    gauge = P.GaugeField(geom, links)
+    cfg = P.GmresConfig(restart_len=10, restarts=30, tol=1e-10)
+    reps = []
+    for layout in (1, 2):
+        f = P.BlockSpinorField.zeros(geom.n_sites, 6, P.Layout(layout), geom=geom)
+        f.set_ksi(eta)
+        reps.append(P.solve_dirac(P.DiracParams(m0=0.1), gauge, None, f, cfg, odd_even=True))
+    f2 = P.BlockSpinorField.zeros(geom.n_sites, 6, P.Layout.COMPONENT_MAJOR, geom=geom)
+    f2.set_ksi(eta)
+    foreign = SimpleNamespace(n_sites=f2.n_sites, s=f2.s, b=f2.b, layout=2, data=f2.data.copy(), geom=geom)
+    eta_dirac = P.apply_dirac(P.DiracParams(m0=0.1), gauge, None, foreign)
+    assert np.array_equal(eta_dirac.ksi(), P.apply_dirac(P.DiracParams(m0=0.1), gauge, None, f2).ksi())
+    assert reps[0].iterations == reps[1].iterations
+    assert np.array_equal(reps[0].psi.ksi(), reps[1].psi.ksi())
+    assert reps[0].psi.layout == 1 and reps[1].psi.layout == 2
