@@ -265,6 +265,20 @@ int b200wd_gmres_arnoldi(const b200wd_gmres_state* st, const b200wd_operator* op
                          int64_t n_sites, const void* const* z, double* relnorm_host,
                          void* stream);
 
+/* A whole restart cycle of Arnoldi steps (gmres.py:218-224) enqueued with no
+ * host round trip: steps j = 0 .. m_run-1 as in b200wd_gmres_arnoldi, each
+ * followed by a record kernel that stores the b relnorms in row j of
+ * hist_dev (double [m_run][b]) and sets ctl_dev[0] (int) once every rhs is
+ * below tol (never when fixed != 0); kernels of later steps see the flag and
+ * do nothing.  ctl_dev[1] = steps completed.  One synchronisation at the end
+ * copies ctl_dev (2 ints) and the used rows of hist_dev to ctl_host /
+ * hist_host.  Same kernels in the same order as the per-step call, so the
+ * results are bit-identical.  B200WD_ERR_UNSUPPORTED if the cooperative
+ * sweep cannot be launched (use b200wd_gmres_arnoldi). */
+int b200wd_gmres_cycle(const b200wd_gmres_state* st, const b200wd_operator* op, int32_t m_run,
+                       int64_t n_sites, const void* const* z, double tol, int32_t fixed, void* ctl_dev,
+                       void* hist_dev, int32_t* ctl_host, double* hist_host, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -122,6 +122,7 @@ SIGNATURES = {
     "b200wd_gmres_update": [_ST, _i32, _i64, _i32, C.POINTER(_vp), _vp, _vp],
     "b200wd_operator_apply": [_OP, _i32, _vp, _vp, _vp, _vp],
     "b200wd_gmres_arnoldi": [_ST, _OP, _i32, _i64, C.POINTER(_vp), _vp, _vp],
+    "b200wd_gmres_cycle": [_ST, _OP, _i32, _i64, C.POINTER(_vp), _dbl, _i32, _vp, _vp, _vp, _vp, _vp],
 }
 RESTYPES = {"b200wd_last_error": C.c_char_p, "b200wd_reduce_scratch_bytes": _i64}
 

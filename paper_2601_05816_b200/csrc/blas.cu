@@ -440,7 +440,8 @@ __device__ __forceinline__ double2 fold_partials(const double2* part, double2* r
   return red[r];
 }
 
-__global__ void arnoldi_sweep_kernel(int j, int64_t n, int s, ZList zl, double2* w, GState g) {
+__global__ void arnoldi_sweep_kernel(int j, int64_t n, int s, ZList zl, double2* w, GState g, const int* stop) {
+  if (stop != nullptr && *static_cast<const volatile int*>(stop) != 0) return;  // cycle already converged
   extern __shared__ double2 red[];
   cg::grid_group grid = cg::this_grid();
   const int b = blockDim.x, r = threadIdx.x, y = threadIdx.y;
@@ -670,7 +671,8 @@ static bool sweep_single_launch(const b200wd_gmres_state* st, int j, int64_t n_s
   int jj = j, ss = s;
   int64_t nn = n_sites;
   double2* wp = static_cast<double2*>(w);
-  void* args[] = {&jj, &nn, &ss, &zl, &wp, &g};
+  const int* stop = g_hop_stop;
+  void* args[] = {&jj, &nn, &ss, &zl, &wp, &g, &stop};
   if (cudaLaunchCooperativeKernel((const void*)arnoldi_sweep_kernel, dim3(grid), blk, args, smem,
                                   as_stream(stream)) == cudaSuccess)
     return true;
@@ -707,6 +709,81 @@ extern "C" int b200wd_gmres_arnoldi(const b200wd_gmres_state* st, const b200wd_o
       set_error("b200wd_gmres_arnoldi: %s", cudaGetErrorString(e));
       return B200WD_ERR_CUDA;
     }
+  }
+  return B200WD_OK;
+}
+
+// After Arnoldi step j of a device-driven cycle: store relnorm into row j of
+// the cycle history and raise the stop flag when every rhs is below tol (the
+// reference's `relnorm.max() < tol`, gmres.py:222-224; a NaN never converges).
+// ctl[0]: stop flag, ctl[1]: steps completed in this cycle.
+__global__ void gmres_record_kernel(int j, int b, const double* __restrict__ relnorm, double tol, int fixed,
+                                    double* hist, int* ctl) {
+  if (*static_cast<volatile int*>(ctl) != 0) return;
+  __shared__ int all_below;
+  if (threadIdx.x == 0) all_below = 1;
+  __syncthreads();
+  for (int r = threadIdx.x; r < b; r += blockDim.x) {
+    const double v = relnorm[r];
+    hist[(int64_t)j * b + r] = v;
+    if (!(v < tol)) all_below = 0;  // benign race: every writer stores 0
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctl[1] = j + 1;
+    if (!fixed && all_below) ctl[0] = 1;
+  }
+}
+
+namespace {
+struct StopScope {  // routes the hop launchers' stop flag for the calls in scope
+  explicit StopScope(const int* f) { g_hop_stop = f; }
+  ~StopScope() { g_hop_stop = nullptr; }
+};
+}  // namespace
+
+extern "C" int b200wd_gmres_cycle(const b200wd_gmres_state* st, const b200wd_operator* op, int32_t m_run,
+                                  int64_t n_sites, const void* const* z, double tol, int32_t fixed, void* ctl_dev,
+                                  void* hist_dev, int32_t* ctl_host, double* hist_host, void* stream) {
+  CHECK_STATE(st);
+  B200WD_REQUIRE(op != nullptr && z != nullptr && ctl_dev && hist_dev && ctl_host && hist_host, "NULL pointer");
+  B200WD_REQUIRE(1 <= m_run && m_run <= st->m, "cycle length %d outside [1, %d]", m_run, st->m);
+  B200WD_REQUIRE(op->dtype == B200WD_C128, "the device GMRES runs in complex128");
+  const int32_t s = 12;
+  CHECK_FIELD(n_sites, s, st->b);
+  for (int p = 0; p <= m_run; ++p) B200WD_REQUIRE(z[p] != nullptr, "basis pointer %d is NULL", p);
+  cudaStream_t cs = as_stream(stream);
+  int* ctl = static_cast<int*>(ctl_dev);
+  double* hist = static_cast<double*>(hist_dev);
+  if (cudaMemsetAsync(ctl, 0, 2 * sizeof(int), cs) != cudaSuccess) return check_launch("b200wd_gmres_cycle");
+  {
+    StopScope scope(ctl);
+    for (int j = 0; j < m_run; ++j) {
+      void* w = const_cast<void*>(z[j + 1]);
+      const double* sig = static_cast<const double*>(st->sigma) + (int64_t)j * st->b;
+      if (int rc = b200wd_operator_apply(op, st->b, z[j], w, sig, stream)) return rc;
+      if (!sweep_single_launch(st, j, n_sites, s, z, w, stream)) {
+        // the per-pass kernels carry no stop flag: this path needs the
+        // cooperative sweep (the caller falls back to per-step calls)
+        if (j == 0) {
+          set_error("b200wd_gmres_cycle: cooperative sweep unavailable");
+          return B200WD_ERR_UNSUPPORTED;
+        }
+        set_error("b200wd_gmres_cycle: cooperative sweep failed at step %d", j);
+        return B200WD_ERR_CUDA;
+      }
+      gmres_record_kernel<<<1, 128, 0, cs>>>(j, st->b, static_cast<const double*>(st->relnorm), tol, fixed, hist,
+                                             ctl);
+      if (int rc = check_launch("b200wd_gmres_cycle")) return rc;
+    }
+  }
+  cudaError_t e = cudaMemcpyAsync(ctl_host, ctl, 2 * sizeof(int), cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(hist_host, hist, sizeof(double) * m_run * st->b, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) {
+    set_error("b200wd_gmres_cycle: %s", cudaGetErrorString(e));
+    return B200WD_ERR_CUDA;
   }
   return B200WD_OK;
 }

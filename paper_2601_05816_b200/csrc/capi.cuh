@@ -11,6 +11,9 @@ namespace b200wd {
 
 void set_error(const char* fmt, ...);
 
+// stop flag of the GMRES cycle being enqueued on this thread (dirac.cu)
+extern thread_local const int* g_hop_stop;
+
 inline int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

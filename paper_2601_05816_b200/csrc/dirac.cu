@@ -18,6 +18,10 @@
 
 namespace b200wd {
 
+// Stop flag of the GMRES cycle being enqueued on this thread (b200wd_gmres_cycle
+// sets it around its operator applications); nullptr everywhere else.
+thread_local const int* g_hop_stop = nullptr;
+
 static int fill_params(HopParams& p, const b200wd_lattice* lat, int32_t dtype, int32_t b, int32_t parity) {
   B200WD_REQUIRE(lat != nullptr, "lattice descriptor is NULL");
   for (int d = 0; d < 4; ++d)
@@ -40,6 +44,7 @@ static int fill_params(HopParams& p, const b200wd_lattice* lat, int32_t dtype, i
   p.n_src = parity < 0 ? p.n : p.n / 2;
   p.n_dst = p.n_src;
   p.nf = parity < 0 ? p.per_t : p.per_t / 2;
+  p.stop = g_hop_stop;
   return B200WD_OK;
 }
 

@@ -53,6 +53,7 @@ template <> struct HopMinBlocks<float> { static constexpr int value = B200WD_MIN
 template <typename R, int V, int B>
 __global__ void __launch_bounds__(kHopThreads, HopMinBlocks<R>::value) hop_kernel(const HopParams p) {
   using C = cx<R>;
+  if (hop_stopped(p)) return;
   const int64_t d = p.d_begin + (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
   if (d >= p.d_end) return;
   const int b = B > 0 ? B : p.b;
@@ -359,6 +360,7 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
   using Sh = RingShape<R, V, B, NB, PAR>;
   constexpr int F = Sh::F;
   constexpr int KST = 8 * B;
+  if (hop_stopped(p)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   C* ring = reinterpret_cast<C*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + S * Sh::SLOT);

@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(Ring2Shape<R, V, B, NB>::NT) hop_ring2_kernel(
   using Sh = Ring2Shape<R, V, B, NB>;
   constexpr int KST = 8 * B;
   constexpr int SEG = 8 * NB;  // sites per line
+  if (hop_stopped(p)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   C* ring = reinterpret_cast<C*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + S * Sh::SLOT);

@@ -50,7 +50,14 @@ struct HopParams {
   // the blocks return as own blocks one patch slice later)
   int32_t hint_t1;
   int32_t hint_tm1;  // 1: the t-1 neighbour tile (its last use) is copied evict-first
+  // device stop flag of a GMRES cycle enqueued without host round trips
+  // (b200wd_gmres_cycle): when *stop != 0 at launch the kernel does nothing
+  const int* stop;
 };
+
+__device__ __forceinline__ bool hop_stopped(const HopParams& p) {
+  return p.stop != nullptr && *static_cast<const volatile int*>(p.stop) != 0;
+}
 
 // y = M t for the two packed Hermitian 6x6 blocks of one site (fields.py:212-247:
 // lower triangle, row-major, element (i,j), i >= j, at i(i+1)/2 + j)

@@ -261,6 +261,7 @@ __global__ void __launch_bounds__(TsShape<R, V, B, NB, LY>::NT, TsShape<R, V, B,
   using Sh = TsShape<R, V, B, NB, LY>;
   constexpr int KST = 8 * B;
   constexpr int SEG = Sh::SEG;
+  if (hop_stopped(p)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   C* ring = reinterpret_cast<C*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + S * Sh::SLOT);

@@ -35,6 +35,9 @@ from .oddeven import SchurOperator
 # B200WD_PY_ARNOLDI=1 issues the Arnoldi step kernel by kernel from Python
 # (the multi-rank path always does, to all-reduce between passes).
 NATIVE_ARNOLDI = os.environ.get("B200WD_PY_ARNOLDI", "0") != "1"
+# whole restart cycles enqueued by the library with a device-side stop flag
+# (b200wd_gmres_cycle); B200WD_STEP_ARNOLDI=1 keeps one ABI call per step
+NATIVE_CYCLE = os.environ.get("B200WD_STEP_ARNOLDI", "0") != "1"
 log = logging.getLogger(__name__)
 _TINY = 1e-300
 
@@ -198,6 +201,12 @@ def gmres_solve(op, eta, psi0, cfg: GmresConfig) -> GmresResult:
     if reduce is None and not cfg.reorthogonalize and NATIVE_ARNOLDI and hasattr(dop, "native_operator"):
         nop = dop.native_operator(z[0])
     rel_host = torch.empty(b, dtype=torch.float64, pin_memory=True) if nop is not None else None
+    cycle = None
+    if nop is not None and NATIVE_CYCLE:  # device-side stop test: one host round trip per cycle
+        cycle = {"ctl": torch.zeros(2, dtype=torch.int32, device=dev),
+                 "hist": torch.empty((m, b), dtype=torch.float64, device=dev),
+                 "ctl_host": torch.zeros(2, dtype=torch.int32, pin_memory=True),
+                 "hist_host": torch.empty((m, b), dtype=torch.float64, pin_memory=True)}
 
     block_norm2_device(d_eta, st.dot)
     allreduce()
@@ -219,7 +228,23 @@ def gmres_solve(op, eta, psi0, cfg: GmresConfig) -> GmresResult:
         if not cfg.fixed_iterations and rel.max() < cfg.tol:
             finish = True
         j_done = 0
-        if not finish:
+        if not finish and cycle is not None:
+            rc = L.b200wd_gmres_cycle(st.ref, ctypes.byref(nop), m, n, zptrs, float(cfg.tol),
+                                      int(bool(cfg.fixed_iterations)), cycle["ctl"].data_ptr(),
+                                      cycle["hist"].data_ptr(), cycle["ctl_host"].data_ptr(),
+                                      cycle["hist_host"].data_ptr(), stream)
+            if rc == _lib.ERR_UNSUPPORTED and iterations == 0:
+                cycle = None  # no cooperative sweep here: per-step calls below
+            else:
+                chk(rc, "gmres_cycle")
+                stop, j_done = (int(v) for v in cycle["ctl_host"].numpy())
+                hist = cycle["hist_host"].numpy()
+                for jj in range(j_done):
+                    history.append(hist[jj].copy())
+                iterations += j_done
+                rel = hist[j_done - 1].copy()
+                finish = bool(stop)
+        if not finish and cycle is None:
             for j in range(m):
                 if nop is not None:
                     chk(L.b200wd_gmres_arnoldi(st.ref, ctypes.byref(nop), j, n, zptrs, rel_host.data_ptr(),

@@ -293,3 +293,34 @@ def test_solve_layouts_and_foreign_fields_agree():
     assert reps[0].iterations == reps[1].iterations
     assert np.array_equal(reps[0].psi.ksi(), reps[1].psi.ksi())
     assert reps[0].psi.layout == 1 and reps[1].psi.layout == 2
+
+
+@pytest.mark.parametrize("case", ["full", "oe_clover", "fixed"])
+def test_device_cycle_bitwise_equals_per_step(case, monkeypatch):
+    """b200wd_gmres_cycle (a whole restart cycle enqueued with a device-side
+    stop flag, one host round trip per cycle) runs the per-step call's kernels
+    in the same order: identical iterations, histories and solutions, also
+    when convergence falls mid-cycle (later kernels see the flag and exit)."""
+    import paper_2601_05816_b200.gmres as G
+    dims = (8, 4, 4, 4)
+    geom = P.LatticeGeometry(dims)
+    links = O.flip_time_boundary(O.near_unit_gauge(dims, 0.3, 81), dims)
+    clover = P.CloverField(geom, O.pack_clover(O.gen_clover_random(dims, 0.05, 82))) if "clover" in case else None
+    eta = host_field(O.gen_spinor(512, 6, 83), 2, geom)
+    if case == "fixed":
+        cfg = P.GmresConfig(restart_len=7, restarts=3, fixed_iterations=True)
+    else:
+        cfg = P.GmresConfig(restart_len=16, restarts=20, tol=1e-10)
+    runs = []
+    for cyc in (True, False):
+        monkeypatch.setattr(G, "NATIVE_CYCLE", cyc)
+        runs.append(P.solve_dirac(P.DiracParams(m0=0.1), P.GaugeField(geom, links), clover, eta, cfg,
+                                  odd_even=case.startswith("oe")))
+    a, b = runs
+    assert a.iterations == b.iterations
+    if case == "fixed":
+        assert a.iterations == 21
+    else:
+        assert a.iterations % 16 != 0  # converged inside a cycle
+    assert np.array_equal(np.array(a.result.history), np.array(b.result.history))
+    assert np.array_equal(a.psi.ksi(), b.psi.ksi())
