@@ -30,6 +30,8 @@ _LAZY = {
     "upload_gauge": "device",
     "TSplitComm": "tsplit",
     "MultiRankExecutor": "multirank", "apply_dirac_multirank": "multirank", "EpochStats": "multirank",
+    "RunConfig": "config", "ConfigError": "config", "parse_config": "config", "load_config": "config",
+    "canonical": "config", "config_hash": "config",
     "arithmetic_intensity": "perf", "theoretical_perf": "perf", "read_write_ratio": "perf",
     "effective_bandwidth": "perf", "arch_efficiency": "perf", "CounterSample": "perf",
 }

@@ -1,20 +1,26 @@
-"""Command line: the reference's measurement surface on the B200 path.
+"""Command line: the reference CLI (``lqcdlab``, cli.py:1-424) on the B200 path.
 
-``python -m paper_2601_05816_b200 <command> ...`` with the reference CLI's
-record formats (cli.py:96-184):
+``python -m paper_2601_05816_b200 <command> [--config FILE] [--set KEY=VALUE ...]``
+takes the reference's run-config files and overrides (``config.py``; the
+canonical text and hash are the reference's for reference keys) and writes
+the reference's records:
 
-* ``bench-dirac``: per (nrhs, layout) the median D_W apply time and the
+* ``bench-dirac [--b-list ...] [--layout-list ...] [--reps N]``: per
+  (nrhs, layout) the median apply time through the host-field API and the
   reference's record fields (b, layout, seconds, gflops from the 2574
-  flop/site/rhs ledger, ai, bytes, checksums), plus the B200 columns:
-  device-resident time (CUDA events), site*rhs/s, algorithmic HBM GB/s and the
-  fraction of the measured HBM peak.
-* ``solve``: batched GMRES (full or odd-even), writes ``psi.snap`` and
-  ``history.csv`` (iter, rhs, relnorm) and prints the final explicit relnorms.
-* ``gen-fields``: writes gauge / clover / psi snapshots (fields.py:266-337).
+  flop/site/rhs ledger, ai, flops, bytes, checksums), plus the B200 columns:
+  device-resident time (CUDA events), site*rhs/s, algorithmic HBM GB/s and
+  the fraction of the measured HBM peak, dtype;
+* ``solve``: batched GMRES (full or odd-even; ``ranks.grid`` > 1 runs the
+  apply through ``MultiRankExecutor``), writes ``psi.snap`` and
+  ``history.csv`` (iter, rhs, relnorm), prints the final explicit relnorms;
+* ``gen-fields``: gauge / clover / psi snapshots (fields.py:266-337).
 
-Every command first prints the JSON header {version, config_hash, seed, rng}
-(cli.py:60-67).  Exit codes: 0 ok, 1 invalid arguments, 2 numerical
-failure, 3 internal error (cli.py:405-424).
+``oracle-check``, ``stream``, ``roofline`` and ``cost-model`` (the CPU
+model tools) are not part of the B200 path and exit with status 1.  Every
+command first prints the JSON header {version, config_hash, seed, rng}
+(cli.py:60-67).  Exit codes: 0 ok, 1 invalid configuration or arguments,
+2 numerical failure, 3 internal error (cli.py:405-424).
 """
 
 from __future__ import annotations
@@ -31,16 +37,17 @@ import time
 import numpy as np
 
 from . import __version__
-from .fields import (RNG_ALGORITHM, flip_time_boundary, gen_clover, gen_gauge, gen_spinor,
-                     near_unit_gauge, write_clover, write_gauge, write_spinor)
-from .geometry import LatticeGeometry
+from .config import ConfigError, RunConfig, canonical, layout_of, load_config, set_key, validate
+from .fields import (RNG_ALGORITHM, flip_time_boundary, gen_clover, gen_gauge, gen_spinor, near_unit_gauge,
+                     write_clover, write_gauge, write_spinor)
+from .geometry import LatticeGeometry, RankGrid, decompose
 
 
 class NumericalFailure(RuntimeError):
     pass
 
 
-class UsageError(ValueError):
+class UsageError(ConfigError):
     pass
 
 
@@ -53,26 +60,51 @@ def _checksum(data) -> str:
     return hashlib.sha256(np.ascontiguousarray(data).tobytes()).hexdigest()[:16]
 
 
-def _header(args) -> None:
-    text = json.dumps({k: v for k, v in sorted(vars(args).items()) if k != "func"}, default=str)
-    print(json.dumps({"version": __version__, "config_hash": hashlib.sha256(text.encode()).hexdigest()[:12],
-                      "seed": args.seed, "rng": RNG_ALGORITHM}))
+def _header(cfg: RunConfig) -> None:
+    print(json.dumps({"version": __version__,
+                      "config_hash": hashlib.sha256(canonical(cfg).encode()).hexdigest()[:12],
+                      "seed": cfg.seed, "rng": RNG_ALGORITHM}))
+
+
+def _runconfig(args) -> RunConfig:
+    """--config file, then every --set KEY=VALUE, then validation (cli.py:70-78)."""
+    cfg = load_config(args.config) if args.config else RunConfig()
+    for item in args.set or []:
+        key, sep, value = item.partition("=")
+        if not sep:
+            raise ConfigError(f"--set needs key=value, got {item!r}")
+        set_key(cfg, key.strip(), value.strip())
+    validate(cfg)
+    return cfg
 
 
 def _ints(text: str) -> list[int]:
     return [int(p) for p in text.replace(",", " ").split()]
 
 
-def _fields(args, b: int, layout: int):
-    geom = LatticeGeometry(tuple(_ints(args.dims)))
-    if args.gauge == "near-unit":
-        gauge = near_unit_gauge(geom, args.eps, args.seed)
+def _out_file(path: str) -> str:
+    if os.path.dirname(path):
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+    return path
+
+
+def _gauge_clover(cfg: RunConfig):
+    geom = LatticeGeometry(tuple(cfg.dims))
+    if cfg.gauge_mode == "near-unit":
+        gauge = near_unit_gauge(geom, cfg.gauge_eps, cfg.seed)
     else:
-        gauge = gen_gauge(geom, args.gauge, seed=args.seed)
-    if args.antiperiodic:
+        gauge = gen_gauge(geom, cfg.gauge_mode, seed=cfg.seed)
+    if cfg.antiperiodic_time:
         gauge = flip_time_boundary(gauge)
-    clover = gen_clover(geom, args.clover, args.clover_scale, seed=args.seed + 1)
-    psi = gen_spinor(geom.n_sites, b, layout, seed=args.seed + 2, geom=geom)
+    clover = gen_clover(geom, cfg.clover_mode, cfg.clover_scale, seed=cfg.seed + 1)
+    return geom, gauge, clover
+
+
+def _problem(cfg: RunConfig, b: int | None = None, layout: int | None = None):
+    """Seeds: gauge = seed, clover = seed+1, spinor = seed+2 (cli.py:81-86)."""
+    geom, gauge, clover = _gauge_clover(cfg)
+    psi = gen_spinor(geom.n_sites, cfg.b if b is None else b, layout_of(cfg) if layout is None else layout,
+                     seed=cfg.seed + 2, geom=geom)
     return geom, gauge, clover, psi
 
 
@@ -81,25 +113,31 @@ def cmd_bench_dirac(args) -> int:
 
     from .device import upload
     from .dirac import FLOPS_PER_SITE_RHS, DiracOperator, DiracParams, account_traffic, compulsory_bytes_per_site
+    from .perf import arithmetic_intensity
 
-    _header(args)
+    cfg = _runconfig(args)
+    _header(cfg)
     peak = 6546.6
     pk = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
     if os.path.exists(pk):
-        peak = float(json.load(open(pk))["hbm_gbs"])
+        with open(pk) as fh:
+            peak = float(json.load(fh)["hbm_gbs"])
+    b_list = _ints(args.b_list) if args.b_list else [cfg.b]
+    layouts = _ints(args.layout_list) if args.layout_list else [cfg.layout]
+    geom, gauge, clover = _gauge_clover(cfg)
+    op = DiracOperator(DiracParams(m0=cfg.m0), gauge, clover, cfg.dtype)
     records = []
-    for b in _ints(args.b_list):
-        for layout in _ints(args.layouts):
-            geom, gauge, clover, psi = _fields(args, b, layout)
-            op = DiracOperator(DiracParams(m0=args.m0), gauge, clover, args.dtype)
-            times = []
+    for b in b_list:
+        for layout in layouts:
+            psi = gen_spinor(geom.n_sites, b, layout, seed=cfg.seed + 2, geom=geom)
             op.apply_host_pipelined(psi)  # warm-up
+            times = []
             for _ in range(args.reps):
                 t0 = time.perf_counter()
                 op.apply_host_pipelined(psi)
                 times.append(time.perf_counter() - t0)
             seconds = statistics.median(times)
-            d = upload(psi, args.dtype)
+            d = upload(psi, cfg.dtype)
             out = d.empty_like()
             op.apply_device(d, out)
             torch.cuda.synchronize()
@@ -111,21 +149,20 @@ def cmd_bench_dirac(args) -> int:
             torch.cuda.synchronize()
             dev_s = e0.elapsed_time(e1) * 1e-3 / args.reps
             flops = FLOPS_PER_SITE_RHS * geom.n_sites * b
-            led = account_traffic(b)
-            alg = compulsory_bytes_per_site(b, args.dtype) * geom.n_sites
+            alg = compulsory_bytes_per_site(b, cfg.dtype) * geom.n_sites
             records.append({
                 "b": b, "layout": layout, "seconds": seconds, "gflops": flops / seconds / 1e9,
-                "ai": FLOPS_PER_SITE_RHS * b / led["bytes_per_site"], "flops": flops,
-                "bytes": led["bytes_per_site"] * geom.n_sites,
+                "ai": float(arithmetic_intensity(b)), "flops": flops,
+                "bytes": account_traffic(b)["bytes_per_site"] * geom.n_sites,
                 "checksums": {"gauge": _checksum(gauge.data), "clover": _checksum(clover.data),
                               "psi": _checksum(psi.data)},
                 "device_seconds": dev_s, "site_rhs_per_s": geom.n_sites * b / dev_s,
-                "hbm_gbs": alg / dev_s / 1e9, "roofline_frac": alg / dev_s / 1e9 / peak, "dtype": args.dtype,
+                "hbm_gbs": alg / dev_s / 1e9, "roofline_frac": alg / dev_s / 1e9 / peak, "dtype": cfg.dtype,
             })
     text = json.dumps({"records": records}, indent=2)
     print(text)
-    if args.out:
-        with open(args.out, "w", encoding="utf-8") as fh:
+    if cfg.out_path:
+        with open(_out_file(cfg.out_path), "w", encoding="utf-8") as fh:
             fh.write(text + "\n")
     return 0
 
@@ -133,19 +170,23 @@ def cmd_bench_dirac(args) -> int:
 def cmd_solve(args) -> int:
     from .dirac import DiracParams
     from .gmres import GmresConfig, solve_dirac
+    from .multirank import MultiRankExecutor
 
-    _header(args)
-    _, gauge, clover, eta = _fields(args, args.b, args.layout)
-    cfg = GmresConfig(restart_len=args.restart_len, restarts=args.restarts, tol=args.tol,
-                      fixed_iterations=args.fixed_iterations)
-    rep = solve_dirac(DiracParams(m0=args.m0), gauge, clover, eta, cfg, odd_even=args.odd_even)
-    psi_path = f"{args.out}psi.snap" if args.out else "psi.snap"
-    hist_path = f"{args.out}history.csv" if args.out else "history.csv"
-    for path in (psi_path, hist_path):
-        if os.path.dirname(path):
-            os.makedirs(os.path.dirname(path), exist_ok=True)
-    write_spinor(psi_path, rep.psi)
-    with open(hist_path, "w", newline="", encoding="utf-8") as fh:
+    cfg = _runconfig(args)
+    _header(cfg)
+    geom, gauge, clover, eta = _problem(cfg)
+    gcfg = GmresConfig(restart_len=cfg.restart_len, restarts=cfg.restarts, tol=cfg.tol,
+                       fixed_iterations=cfg.fixed_iterations)
+    comm = None
+    if any(g > 1 for g in cfg.grid):
+        grid = RankGrid(tuple(cfg.grid))
+        decompose(geom, grid)  # validate before building the executor
+        comm = MultiRankExecutor(grid)
+    rep = solve_dirac(DiracParams(m0=cfg.m0), gauge, clover, eta, gcfg, odd_even=cfg.odd_even, comm=comm)
+    psi_path = f"{cfg.out_path}psi.snap"
+    hist_path = f"{cfg.out_path}history.csv"
+    write_spinor(_out_file(psi_path), rep.psi)
+    with open(_out_file(hist_path), "w", newline="", encoding="utf-8") as fh:
         w = csv.writer(fh)
         w.writerow(["iter", "rhs", "relnorm"])
         for it, rel in enumerate(rep.result.history):
@@ -153,69 +194,61 @@ def cmd_solve(args) -> int:
                 w.writerow([it, r, repr(float(rel[r]))])
     for r, rel in enumerate(rep.full_relnorms):
         print(f"rhs {r}: final explicit relnorm {rel:.6e}")
-    ok = bool(np.all(rep.full_relnorms <= args.tol))
+    ok = bool(np.all(rep.full_relnorms <= cfg.tol))
     print(json.dumps({"iterations": rep.iterations, "odd_even": rep.odd_even,
-                      "converged": ok if not args.fixed_iterations else None, "psi": psi_path, "history": hist_path}))
-    if not args.fixed_iterations and not ok:
-        raise NumericalFailure(f"solver did not reach tol {args.tol:g}; worst relnorm {rep.full_relnorms.max():.3e}")
+                      "converged": ok if not cfg.fixed_iterations else None, "psi": psi_path,
+                      "history": hist_path}))
+    if not cfg.fixed_iterations and not ok:
+        raise NumericalFailure(f"solver did not reach tol {cfg.tol:g}; worst relnorm {rep.full_relnorms.max():.3e}")
     return 0
 
 
 def cmd_gen_fields(args) -> int:
-    _header(args)
-    _, gauge, clover, psi = _fields(args, args.b, args.layout)
-    pre = args.out or ""
+    cfg = _runconfig(args)
+    _header(cfg)
+    _, gauge, clover, psi = _problem(cfg)
+    pre = cfg.out_path
     paths = {"gauge": f"{pre}gauge.snap", "clover": f"{pre}clover.snap", "psi": f"{pre}psi.snap"}
-    for p in paths.values():
-        if os.path.dirname(p):
-            os.makedirs(os.path.dirname(p), exist_ok=True)
-    write_gauge(paths["gauge"], gauge)
-    write_clover(paths["clover"], clover)
-    write_spinor(paths["psi"], psi)
+    write_gauge(_out_file(paths["gauge"]), gauge)
+    write_clover(_out_file(paths["clover"]), clover)
+    write_spinor(_out_file(paths["psi"]), psi)
     print(json.dumps({"files": paths, "checksums": {"gauge": _checksum(gauge.data), "clover": _checksum(clover.data),
                                                     "psi": _checksum(psi.data)}}, indent=2))
     return 0
 
 
+def cmd_not_provided(args) -> int:
+    raise UsageError(f"'{args.command}' is a CPU-model tool of the reference CLI and is not part of the B200 "
+                     "path (DESIGN.md section 7)")
+
+
 def build_parser() -> argparse.ArgumentParser:
-    p = _Parser(prog="paper_2601_05816_b200")
+    p = _Parser(prog="paper_2601_05816_b200", description=__doc__)
     sub = p.add_subparsers(dest="command", required=True, parser_class=_Parser)
 
-    def common(sp):
-        sp.add_argument("--dims", default="8 8 8 8", help="T X Y Z (T slowest)")
-        sp.add_argument("--m0", type=float, default=0.1)
-        sp.add_argument("--seed", type=int, default=0, help="gauge=seed, clover=seed+1, psi=seed+2 (cli.py:81-86)")
-        sp.add_argument("--gauge", choices=["unit", "random", "near-unit"], default="random")
-        sp.add_argument("--eps", type=float, default=0.3)
-        sp.add_argument("--antiperiodic", action="store_true", help="antiperiodic T (U_0 flipped on the last slice)")
-        sp.add_argument("--clover", choices=["zero", "random"], default="zero")
-        sp.add_argument("--clover-scale", type=float, default=0.1)
-        sp.add_argument("--out", default=None)
+    def runconfig_args(sp):
+        sp.add_argument("--config", help="path to a key = value config file")
+        sp.add_argument("--set", action="append", metavar="KEY=VALUE", help="override one config key (repeatable)")
 
-    sp = sub.add_parser("bench-dirac")
-    common(sp)
-    sp.add_argument("--b-list", default="1 2 4 8 16")
-    sp.add_argument("--layouts", default="2")
-    sp.add_argument("--reps", type=int, default=5)
-    sp.add_argument("--dtype", choices=["c128", "c64"], default="c128")
+    sp = sub.add_parser("bench-dirac", help="time the operator over b/layout sweeps")
+    runconfig_args(sp)
+    sp.add_argument("--b-list", help="comma/space-separated b values to sweep")
+    sp.add_argument("--layout-list", help="comma/space-separated layouts to sweep")
+    sp.add_argument("--reps", type=int, default=3, help="timed repetitions (median)")
     sp.set_defaults(func=cmd_bench_dirac)
 
-    sp = sub.add_parser("solve")
-    common(sp)
-    sp.add_argument("--b", type=int, default=4)
-    sp.add_argument("--layout", type=int, default=2)
-    sp.add_argument("--restart-len", type=int, default=30)
-    sp.add_argument("--restarts", type=int, default=67)
-    sp.add_argument("--tol", type=float, default=1e-10)
-    sp.add_argument("--fixed-iterations", action="store_true")
-    sp.add_argument("--odd-even", action="store_true")
+    sp = sub.add_parser("solve", help="run the batched solver on a seeded problem")
+    runconfig_args(sp)
     sp.set_defaults(func=cmd_solve)
 
-    sp = sub.add_parser("gen-fields")
-    common(sp)
-    sp.add_argument("--b", type=int, default=4)
-    sp.add_argument("--layout", type=int, default=2)
+    sp = sub.add_parser("gen-fields", help="write seeded gauge/clover/spinor snapshots")
+    runconfig_args(sp)
     sp.set_defaults(func=cmd_gen_fields)
+
+    for name in ("oracle-check", "stream", "roofline", "cost-model"):
+        sp = sub.add_parser(name, help="reference CPU-model tool (not part of the B200 path)")
+        sp.add_argument("rest", nargs=argparse.REMAINDER)
+        sp.set_defaults(func=cmd_not_provided)
     return p
 
 
@@ -223,10 +256,17 @@ def main(argv=None) -> int:
     try:
         args = build_parser().parse_args(argv)
         return args.func(args)
-    except (UsageError, ValueError) as exc:
+    except (ConfigError, ValueError, NotImplementedError) as exc:
         print(f"error: {exc}", file=sys.stderr)
         return 1
-    except NumericalFailure as exc:
+    except (NumericalFailure, np.linalg.LinAlgError) as exc:
+        print(f"numerical failure: {exc}", file=sys.stderr)
+        return 2
+    except RuntimeError as exc:
+        from ._lib import B200Unavailable
+        if isinstance(exc, B200Unavailable):
+            print(f"internal error: {exc}", file=sys.stderr)
+            return 3
         print(f"numerical failure: {exc}", file=sys.stderr)
         return 2
     except Exception as exc:  # noqa: BLE001 - map to the reference's internal-error code

@@ -82,10 +82,10 @@ class MultiRankExecutor:
         self._plan, self._plan_key = (slabs, CudaHaloKernels()), key
         return self._plan
 
-    def apply_device(self, params, gauge, clover, psi: DeviceField, out: DeviceField | None = None) -> DeviceField:
-        """Device fields in and out (whole lattice)."""
-        import torch
-
+    def apply_device(self, params, gauge, clover, psi: DeviceField, out: DeviceField | None = None,
+                     scale=None) -> DeviceField:
+        """Device fields in and out (whole lattice); ``scale`` (device, b
+        doubles) multiplies each rhs of the result, as in DiracOperator."""
         if psi.n_sites != gauge.geom.n_sites or psi.s != SPINOR_LEN:
             raise ValueError(f"field has {psi.n_sites} sites / s={psi.s}, lattice has {gauge.geom.n_sites} sites")
         slabs, k = self._plan_for(gauge, clover, psi.dtype)
@@ -106,12 +106,11 @@ class MultiRankExecutor:
             chi_in = faces[(r - 1) % ranks][1]  # chi of rank r-1's last slice
             T = lg.dims[0]
             if T > 2:
-                hop_device(lat, dt, b, -1, dg, x, y, x, alpha, -1.0, None, 1, T - 1, clover=dc, clover_mode=1)
+                hop_device(lat, dt, b, -1, dg, x, y, x, alpha, -1.0, scale, 1, T - 1, clover=dc, clover_mode=1)
             for t in (0, T - 1):
-                hop_device(lat, dt, b, -1, dg, x, y, x, alpha, -1.0, None, t, t + 1, lam_in, chi_in, clover=dc,
+                hop_device(lat, dt, b, -1, dg, x, y, x, alpha, -1.0, scale, t, t + 1, lam_in, chi_in, clover=dc,
                            clover_mode=1)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t_start
+        wall = time.perf_counter() - t_start  # host issue time (the device work is asynchronous)
         self.last_stats = [EpochStats(self.epoch, r, 0.0, wall / ranks) for r in range(ranks)]
         self.epoch += 1
         return out
@@ -133,6 +132,35 @@ class MultiRankExecutor:
             perf.append(DiracPerfRecord(time.perf_counter() - t0, psi.n_sites, psi.b, int(psi.layout),
                                         led["flops_per_site"] * psi.n_sites, led["bytes_per_site"] * psi.n_sites))
         return res
+
+
+    def operator(self, params, gauge, clover=None, dtype: str = "c128"):
+        """The Dirac operator applied through this executor (gmres.py:335-339)."""
+        return _ExecutorOp(self, params, gauge, clover)
+
+    def solve_dirac(self, params, gauge, clover, eta, cfg, odd_even: bool = False, psi0=None):
+        """gmres.py:353-385 with comm=this executor: the unpreconditioned solve
+        applies D through the rank slabs; the odd-even Schur system is
+        single-rank, as in the reference."""
+        from .gmres import SolveReport, gmres_solve
+        from .gmres import solve_dirac as single_rank_solve
+        if odd_even:
+            return single_rank_solve(params, gauge, clover, eta, cfg, odd_even=True, psi0=psi0)
+        res = gmres_solve(self.operator(params, gauge, clover), eta, psi0, cfg)
+        return SolveReport(res.psi, res, False, res.final_relnorms, res.iterations)
+
+
+class _ExecutorOp:
+    """GMRES operator view of a MultiRankExecutor (device fields)."""
+
+    allreduce = None
+
+    def __init__(self, ex: MultiRankExecutor, params, gauge, clover):
+        self.ex, self.params, self.gauge, self.clover = ex, params, gauge, clover
+        self.n_sites = gauge.geom.n_sites
+
+    def apply_device(self, v: DeviceField, out: DeviceField | None = None, scale=None) -> DeviceField:
+        return self.ex.apply_device(self.params, self.gauge, self.clover, v, out, scale)
 
 
 def apply_dirac_multirank(params, gauge, clover, psi, grid: RankGrid, mode: str = "sequential",

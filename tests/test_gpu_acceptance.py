@@ -131,3 +131,18 @@ def test_multirank_executor_matches_single_rank(ranks, with_clover):
     assert len(ex.last_stats) == ranks
     via_comm = P.apply_dirac(params, gauge, clover, psi, comm=P.MultiRankExecutor(P.RankGrid((ranks, 1, 1, 1))))
     assert np.array_equal(via_comm.ksi(), got.ksi())
+
+
+def test_multirank_executor_full_solve():
+    """solve_dirac(..., comm=MultiRankExecutor(grid)) (gmres.py:353-385): the
+    unpreconditioned solve applies D through the rank slabs."""
+    dims = (8, 4, 4, 4)
+    geom = P.LatticeGeometry(dims)
+    gauge = P.flip_time_boundary(P.near_unit_gauge(geom, 0.3, 91))
+    eta = P.gen_spinor(geom.n_sites, 3, P.Layout.COMPONENT_MAJOR, seed=92, geom=geom)
+    cfg = P.GmresConfig(restart_len=20, restarts=20, tol=1e-10)
+    params = P.DiracParams(m0=0.1)
+    ref = P.solve_dirac(params, gauge, None, eta, cfg)
+    got = P.solve_dirac(params, gauge, None, eta, cfg, comm=P.MultiRankExecutor(P.RankGrid((4, 1, 1, 1))))
+    assert abs(got.iterations - ref.iterations) <= 1 and np.all(got.full_relnorms <= 1e-10)
+    assert np.abs(got.psi.ksi() - ref.psi.ksi()).max() / np.abs(ref.psi.ksi()).max() < 1e-8
