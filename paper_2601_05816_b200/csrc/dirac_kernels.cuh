@@ -44,14 +44,16 @@ constexpr int kHopThreads = B200WD_HOP_THREADS;
 #ifndef B200WD_MINB_C64
 #define B200WD_MINB_C64 4
 #endif
-template <typename R> struct HopMinBlocks;
-template <> struct HopMinBlocks<double> { static constexpr int value = B200WD_MINB_C128; };
-template <> struct HopMinBlocks<float> { static constexpr int value = B200WD_MINB_C64; };
+// c128 nrhs 1 measured faster with a 2-block target (0.0353 vs 0.0368 ms on
+// 16^3x32; nrhs 2 equal, nrhs 3 and c64 slower: profiles/r1_tstream_tuning.txt)
+template <typename R, int B> struct HopMinBlocks;
+template <int B> struct HopMinBlocks<double, B> { static constexpr int value = B == 1 ? 2 : B200WD_MINB_C128; };
+template <int B> struct HopMinBlocks<float, B> { static constexpr int value = B200WD_MINB_C64; };
 
 // B > 0: rhs count known at compile time (all component / link strides are
 // immediates); B == 0: runtime rhs count.
 template <typename R, int V, int B>
-__global__ void __launch_bounds__(kHopThreads, HopMinBlocks<R>::value) hop_kernel(const HopParams p) {
+__global__ void __launch_bounds__(kHopThreads, HopMinBlocks<R, B>::value) hop_kernel(const HopParams p) {
   using C = cx<R>;
   if (hop_stopped(p)) return;
   const int64_t d = p.d_begin + (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
