@@ -16,8 +16,11 @@ the reference's records:
   ``history.csv`` (iter, rhs, relnorm), prints the final explicit relnorms;
 * ``gen-fields``: gauge / clover / psi snapshots (fields.py:266-337).
 
-``oracle-check``, ``stream``, ``roofline`` and ``cost-model`` (the CPU
-model tools) are not part of the B200 path and exit with status 1.  Every
+* ``oracle-check [--corrupt-gauge]``: invariant suites evaluated with the
+  device kernels (unitarity, free field, gamma5-hermiticity, Schur identity).
+
+``stream``, ``roofline`` and ``cost-model`` (the CPU model tools) are not part
+of the B200 path and exit with status 1.  Every
 command first prints the JSON header {version, config_hash, seed, rng}
 (cli.py:60-67).  Exit codes: 0 ok, 1 invalid configuration or arguments,
 2 numerical failure, 3 internal error (cli.py:405-424).
@@ -217,6 +220,97 @@ def cmd_gen_fields(args) -> int:
     return 0
 
 
+def cmd_oracle_check(args) -> int:
+    """Invariant suites of the B200 operators, evaluated with device kernels
+    (cli.py:190-268 runs dense-matrix suites on the CPU; here every suite is a
+    property that needs no CPU reference): link unitarity, the free-field
+    identity D psi = m0 psi (unit links, constant psi), gamma5-hermiticity
+    <phi, g5 D psi> = <g5 D phi, psi> at nrhs 1 and 8, and the Schur
+    complement identity (D x)_e = S v_e, (D x)_o = 0 for x = (v_e, -D_oo^-1
+    D_oe v_e).  Any failing suite -> exit status 2."""
+    import torch
+
+    from .device import DeviceField, upload
+    from .dirac import DiracOperator, DiracParams
+    from .fields import BlockSpinorField, GaugeField
+    from .oddeven import SchurOperator, device_merge, device_split
+
+    cfg = _runconfig(args)
+    _header(cfg)
+    geom, gauge, clover = _gauge_clover(cfg)
+    if args.corrupt_gauge:
+        gauge = GaugeField(geom, gauge.data.copy())
+        gauge.data[0, 0, 0, 0] += 0.5
+    params = DiracParams(m0=cfg.m0)
+    tol = 1e-12 if cfg.dtype == "c128" else 1e-5
+    g5 = torch.tensor([1.0] * 6 + [-1.0] * 6, dtype=torch.float64)
+    failures = []
+
+    def suite(name: str, fn) -> None:
+        try:
+            print(f"{name}: PASS ({fn()})")
+        except Exception as exc:  # report, keep running the other suites
+            print(f"{name}: FAIL ({exc})")
+            failures.append(name)
+
+    def unitarity():
+        links = gauge.data
+        if cfg.antiperiodic_time:  # undo the boundary sign before the SU(3) test
+            links = flip_time_boundary(GaugeField(geom, links)).data
+        GaugeField(geom, links).validate()
+        return "links unitary, det 1" + (" (up to the antiperiodic T sign)" if cfg.antiperiodic_time else "")
+
+    def free_field():
+        unit = gen_gauge(geom, "unit")
+        psi = BlockSpinorField.zeros(geom.n_sites, 2, layout_of(cfg), geom=geom)
+        psi.set_ksi(np.ones((geom.n_sites, 12, 2), dtype=np.complex128))
+        eta = DiracOperator(params, unit, None, cfg.dtype)(psi)
+        err = float(np.abs(eta.ksi() - params.m0 * psi.ksi()).max())
+        if err > (1e-14 if cfg.dtype == "c128" else 1e-6):
+            raise NumericalFailure(f"max err {err:.3e}")
+        return f"max err {err:.3e}"
+
+    def gamma5(b: int):
+        def run():
+            op = DiracOperator(params, gauge, clover, cfg.dtype)
+            phi = upload(gen_spinor(geom.n_sites, b, 2, seed=cfg.seed + 3, geom=geom), cfg.dtype)
+            psi = upload(gen_spinor(geom.n_sites, b, 2, seed=cfg.seed + 4, geom=geom), cfg.dtype)
+            g = g5.to(phi.data.device).view(1, 12, 1, 1)
+            dphi, dpsi = op.apply_device(phi).data, op.apply_device(psi).data
+            lhs = (phi.data.conj() * g * dpsi).sum(dim=(0, 1, 2))
+            rhs = ((g * dphi).conj() * psi.data).sum(dim=(0, 1, 2))
+            err = float(((lhs - rhs).abs().max() / lhs.abs().max()).item())
+            if err > tol:
+                raise NumericalFailure(f"rel err {err:.3e}")
+            return f"rel err {err:.3e}"
+        return run
+
+    def schur_identity():
+        schur = SchurOperator(params, gauge, clover, keep_parity=0, dtype=cfg.dtype)
+        dirac = DiracOperator(params, gauge, clover, cfg.dtype)
+        half = geom.n_sites // 2
+        v = upload(gen_spinor(half, 2, 2, seed=cfg.seed + 5), cfg.dtype, parity=0)
+        v.geom = geom
+        zero = DeviceField(torch.zeros_like(v.data), half, geom, 1)
+        x = device_merge(schur.lat, v, schur.reconstruct_device(v, zero), geom)
+        ye, yo = device_split(schur.lat, dirac.apply_device(x))
+        sv = schur.apply_device(v)
+        e1 = float((torch.linalg.vector_norm(ye.data - sv.data) / torch.linalg.vector_norm(sv.data)).item())
+        e2 = float((torch.linalg.vector_norm(yo.data) / torch.linalg.vector_norm(ye.data)).item())
+        if e1 > tol or e2 > tol:
+            raise NumericalFailure(f"rel err {e1:.3e} (even), {e2:.3e} (odd)")
+        return f"rel err {e1:.3e} (even), {e2:.3e} (odd)"
+
+    suite("gauge-unitarity", unitarity)
+    suite("free-field-identity", free_field)
+    suite("gamma5-hermiticity-b1", gamma5(1))
+    suite("gamma5-hermiticity-b8", gamma5(8))
+    suite("schur-identity", schur_identity)
+    if failures:
+        raise NumericalFailure("failing suites: " + ", ".join(failures))
+    return 0
+
+
 def cmd_not_provided(args) -> int:
     raise UsageError(f"'{args.command}' is a CPU-model tool of the reference CLI and is not part of the B200 "
                      "path (DESIGN.md section 7)")
@@ -245,7 +339,12 @@ def build_parser() -> argparse.ArgumentParser:
     runconfig_args(sp)
     sp.set_defaults(func=cmd_gen_fields)
 
-    for name in ("oracle-check", "stream", "roofline", "cost-model"):
+    sp = sub.add_parser("oracle-check", help="invariant suites of the device operators")
+    runconfig_args(sp)
+    sp.add_argument("--corrupt-gauge", action="store_true", help="perturb one link to demonstrate failure detection")
+    sp.set_defaults(func=cmd_oracle_check)
+
+    for name in ("stream", "roofline", "cost-model"):
         sp = sub.add_parser(name, help="reference CPU-model tool (not part of the B200 path)")
         sp.add_argument("rest", nargs=argparse.REMAINDER)
         sp.set_defaults(func=cmd_not_provided)

@@ -83,3 +83,15 @@ def test_solve_writes_history_and_snapshot(tmp_path, capsys, grid):
                "--set", "clover.mode=zero", "--set", f"ranks.grid={grid}", "--set", "solver.restart_len=2",
                "--set", "solver.restarts=1", "--set", "solver.tol=1e-12", "--set", f"output.path={tmp_path}/x"])
     assert rc == 2  # did not converge -> numerical failure
+
+
+@pytest.mark.gpu
+def test_oracle_check_suites(capsys):
+    base = ["oracle-check", "--set", "lattice.dims=4 4 4 8", "--set", "clover.mode=random", "--set", "block.b=3"]
+    assert main(base) == 0
+    out = _lines(capsys)
+    assert sum(line.endswith(")") and ": PASS (" in line for line in out) == 5
+    assert main(base + ["--set", "lattice.antiperiodic_time=true", "--set", "device.dtype=c64"]) == 0
+    capsys.readouterr()
+    assert main(base + ["--corrupt-gauge"]) == 2  # unitarity fails, detected
+    assert "gauge-unitarity: FAIL" in capsys.readouterr().out
