@@ -43,7 +43,7 @@ M0 = 0.1
 METRIC = "D_W apply site*rhs/s (16^3x32, nrhs=16, c128)"
 
 
-PROFILE = ROOT / "profiles" / "r1_ncu_ring_c128_b16_cfg2_s2.json"
+PROFILE = ROOT / "profiles" / "r1_ncu_ring_c128_b16_cfg2_final.json"
 
 
 def profile_traffic():
