@@ -123,7 +123,21 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+#ifndef B200WD_WAIT_HINT_NS
+#define B200WD_WAIT_HINT_NS 0  // experiment: try_wait suspend-time hint (0: none)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+#if B200WD_WAIT_HINT_NS > 0
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "B200WD_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra B200WD_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase), "r"((uint32_t)B200WD_WAIT_HINT_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -133,6 +147,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(phase)
       : "memory");
+#endif
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
