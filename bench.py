@@ -471,7 +471,7 @@ def main():
         from bench_schur import schur_bench
         line["schur"] = schur_bench()  # BASELINE configs[2]: 32^3x64 Schur apply, nrhs=12, c128
         from bench_strong import single_gpu_apply
-        line["strong_base"] = single_gpu_apply()  # BASELINE configs[4] at N=1: 48^3x96, nrhs=12
+        line["strong_base"] = single_gpu_apply(sampler=ClockSampler)  # BASELINE configs[4] at N=1: 48^3x96, nrhs=12
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample()
     print(json.dumps(line))

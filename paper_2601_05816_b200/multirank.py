@@ -133,7 +133,6 @@ class MultiRankExecutor:
                                         led["flops_per_site"] * psi.n_sites, led["bytes_per_site"] * psi.n_sites))
         return res
 
-
     def operator(self, params, gauge, clover=None, dtype: str = "c128"):
         """The Dirac operator applied through this executor (gmres.py:335-339)."""
         return _ExecutorOp(self, params, gauge, clover)

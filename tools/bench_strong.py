@@ -35,8 +35,13 @@ def hbm_peak():
     return float(json.loads(pk.read_text())["hbm_gbs"]) if pk.exists() else 7672.0
 
 
-def single_gpu_apply(gdims=GDIMS, dtypes=("c128", "c64"), b=12, steps=10, warmup=3):
-    """configs[4] at N=1 (the strong-scaling base point): D_W apply records."""
+def single_gpu_apply(gdims=GDIMS, dtypes=("c128", "c64"), b=12, steps=30, warmup=3, sampler=None):
+    """configs[4] at N=1 (the strong-scaling base point): D_W apply records.
+
+    ``ms`` is the sustained rate (back-to-back launches); ``ms_after_idle`` one
+    launch after 1 s of idle GPU.  The two differ because the sustained apply
+    on this lattice reaches the board power limit (1000 W, sw_power_cap,
+    SM clocks ~1635 MHz): ``clocks`` (``sampler``: bench.ClockSampler) shows it."""
     geom = P.LatticeGeometry(tuple(gdims))
     tg = time.perf_counter()
     gauge = P.flip_time_boundary(P.GaugeField(geom, P.near_unit_links(gdims, 0.3, 0, workers=os.cpu_count() or 1)))
@@ -52,6 +57,13 @@ def single_gpu_apply(gdims=GDIMS, dtypes=("c128", "c64"), b=12, steps=10, warmup
             op.apply_device(psi, eta)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        time.sleep(1.0)
+        e0.record()
+        op.apply_device(psi, eta)
+        e1.record()
+        torch.cuda.synchronize()
+        t_idle = e0.elapsed_time(e1) * 1e-3
+        clk = sampler(torch.cuda.current_device()).start() if sampler else None
         e0.record()
         for _ in range(steps):
             op.apply_device(psi, eta)
@@ -59,8 +71,12 @@ def single_gpu_apply(gdims=GDIMS, dtypes=("c128", "c64"), b=12, steps=10, warmup
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) * 1e-3 / steps
         alg = compulsory_bytes_per_site(b, dt) * n
-        out.append({"dtype": dt, "nrhs": b, "ms": round(t * 1e3, 4), "site_rhs_per_s": n * b / t,
-                    "hbm_gbs": round(alg / t / 1e9, 1), "frac": round(alg / t / 1e9 / peak, 4)})
+        rec = {"dtype": dt, "nrhs": b, "ms": round(t * 1e3, 4), "site_rhs_per_s": n * b / t,
+               "hbm_gbs": round(alg / t / 1e9, 1), "frac": round(alg / t / 1e9 / peak, 4),
+               "ms_after_idle": round(t_idle * 1e3, 4), "frac_after_idle": round(alg / t_idle / 1e9 / peak, 4)}
+        if clk:
+            rec["clocks"] = clk.stop()
+        out.append(rec)
         del psi, eta, op
     from paper_2601_05816_b200.device import gauge_cache
     gauge_cache.clear()

@@ -11,6 +11,7 @@ compulsory bytes (24 b + 36) w per site.
 import argparse
 import json
 import sys
+import time
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
@@ -28,6 +29,7 @@ ap.add_argument("--dtypes", nargs="+", default=["c128", "c64"])
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--parity", type=int, default=-1, help="destination parity of a checkerboard hop (-1: full)")
 ap.add_argument("--cold", action="store_true", help="time each launch alone after an L2 flush (512 MB memset)")
+ap.add_argument("--idle", type=float, default=0.0, help="with --cold: seconds the GPU idles before each launch")
 a = ap.parse_args()
 pk = ROOT / "MEASURED_PEAKS.json"
 peak = float(json.loads(pk.read_text())["hbm_gbs"]) if pk.exists() else 6650.0
@@ -62,12 +64,17 @@ for dt in a.dtypes:
             ts = []
             for i in range(a.iters):
                 flush.fill_(i & 255)
+                if a.idle > 0:
+                    torch.cuda.synchronize()
+                    time.sleep(a.idle)
                 e0.record()
                 go(i)
                 e1.record()
                 torch.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1) * 1e-3)
             t = float(np.median(ts))
+            if a.idle > 0:
+                print("  per launch ms:", " ".join(f"{x*1e3:.2f}" for x in ts))
             del flush
         else:
             e0.record()
