@@ -288,14 +288,11 @@ __device__ __forceinline__ int64_t item_nat(int64_t it, const HopParams& p, uint
   const uint32_t tl = (uint32_t)(p.tile_x * p.tile_y);
   const uint32_t q = i % tl;
   i /= tl;
+  const uint32_t t = i % (uint32_t)p.tile_nt;
   const uint32_t tile = i / (uint32_t)p.tile_nt;
   const uint32_t ny = (uint32_t)(p.Y / p.tile_y);
-  const uint32_t nxy = (uint32_t)(p.X / p.tile_x) * ny;
-  // patches of tile_nt slices: t chunk outermost (one chunk when tile_nt = all slices)
-  const uint32_t t = (tile / nxy) * (uint32_t)p.tile_nt + i % (uint32_t)p.tile_nt;
-  const uint32_t xy = tile % nxy;
-  const uint32_t x = (xy / ny) * p.tile_x + q / p.tile_y;
-  const uint32_t y = (xy % ny) * p.tile_y + q % p.tile_y;
+  const uint32_t x = (tile / ny) * p.tile_x + q / p.tile_y;
+  const uint32_t y = (tile % ny) * p.tile_y + q % p.tile_y;
   return (((int64_t)t * p.X + x) * p.Y + y) * lz + zi;
 }
 
@@ -645,20 +642,10 @@ static void choose_tiles(HopParams& p, int F, int NB, size_t bytes_per_field_sit
       }
     }
   }
-  const int32_t nt = (int32_t)((p.d_end - p.d_begin) / per_t_field);
-  static int shape[3] = {-1, 0, 0};  // experiment override B200WD_TILE_SHAPE="tx,ty,nt", read once
-  if (shape[0] < 0) {
-    shape[0] = 0;
-    if (const char* e = getenv("B200WD_TILE_SHAPE")) sscanf(e, "%d,%d,%d", &shape[0], &shape[1], &shape[2]);
-  }
-  if (shape[0] > 0 && shape[1] > 0 && p.X % shape[0] == 0 && p.Y % shape[1] == 0) {
-    best_x = shape[0];
-    best_y = shape[1];
-  }
-  if (best_x == 0 || (best_x == p.X && best_y == p.Y && !(shape[2] > 0 && shape[2] < nt))) return;
+  if (best_x == 0 || (best_x == p.X && best_y == p.Y)) return;
   p.tile_x = best_x;
   p.tile_y = best_y;
-  p.tile_nt = (shape[2] > 0 && nt % shape[2] == 0) ? shape[2] : nt;
+  p.tile_nt = (int32_t)((p.d_end - p.d_begin) / per_t_field);
 }
 
 template <int NB>
@@ -709,8 +696,7 @@ static bool launch_ring_nb(const HopParams& p_in, int64_t nblk, int S, cudaStrea
     // hops of 32^3 x 64 (tools/variants_cmp.sh); for the full-lattice apply on
     // 48^3 x 96 every patch shape tried (1..8 x 48, 48 x 2..8, 6 x 12) was
     // 10-25% slower than the natural order
-    static const int tile_full = ring_knob("B200WD_TILE_FULL", 0);  // experiment: patch the full lattice too
-    if (PAR || tile_full) choose_tiles(p, Sh::F, NB, site_bytes);
+    if (PAR) choose_tiles(p, Sh::F, NB, site_bytes);
     const int64_t slice_bytes = (int64_t)(p.per_t / Sh::F) * (int64_t)site_bytes;
     static const int hints = ring_knob("B200WD_L2HINT", 1);  // read once per process
     p.hint_t1 = hints ? (p.tile_x ? 2 : (slice_bytes > kSliceNoReuse ? 1 : 0)) : 0;
@@ -722,9 +708,11 @@ static bool launch_ring_nb(const HopParams& p_in, int64_t nblk, int S, cudaStrea
     size_t smem = Sh::smem(S);
     while (smem > 227 * 1024 && S > 2) smem = Sh::smem(--S);
     const int64_t ni = n_items_of<NB>(nblk);
-    if (p.tile_x) {
-      if (whole_lines) return launch_ring_kernel<R, V, B, NB, PAR, true, false>(p, ni, S, smem, st);
-      return launch_ring_kernel<R, V, B, NB, PAR, true, true>(p, ni, S, smem, st);
+    if constexpr (PAR) {
+      if (p.tile_x) {
+        if (whole_lines) return launch_ring_kernel<R, V, B, NB, PAR, true, false>(p, ni, S, smem, st);
+        return launch_ring_kernel<R, V, B, NB, PAR, true, true>(p, ni, S, smem, st);
+      }
     }
     if (whole_lines) return launch_ring_kernel<R, V, B, NB, PAR, false, false>(p, ni, S, smem, st);
     return launch_ring_kernel<R, V, B, NB, PAR, false, true>(p, ni, S, smem, st);
