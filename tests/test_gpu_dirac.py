@@ -281,6 +281,45 @@ def test_gmres_clover_matches_reference_golden():
     assert np.abs(d.psi.ksi() - s.psi.ksi()).max() / np.abs(d.psi.ksi()).max() < 1e-7
 
 
+@pytest.mark.parametrize("dims", [(4, 4, 4, 16), (4, 2, 2, 32), (6, 2, 4, 8), (2, 2, 2, 48)])
+@pytest.mark.parametrize("b,dtype,tol", [(4, "c128", 1e-12), (12, "c128", 1e-12), (16, "c128", 1e-12),
+                                         (8, "c64", 1e-5), (16, "c64", 1e-5)])
+def test_dirac_clover_wide_rhs_matches_oracle(dims, b, dtype, tol):
+    """Clover at nrhs >= 4 on ring-shaped lattices (the clover epilogue stays in
+    the generic kernel: profiles/r1_tstream_tuning.txt, clover section)."""
+    geom = P.LatticeGeometry(dims)
+    links = O.flip_time_boundary(O.near_unit_gauge(dims, 0.3, 21), dims)
+    cl = O.gen_clover_random(dims, 0.1, 22)
+    psi = O.gen_spinor(geom.n_sites, b, 23)
+    c64 = dtype == "c64"
+    ref = O.apply_dirac(dims, 0.1, O.round_c64(links) if c64 else links, O.round_c64(cl) if c64 else cl,
+                        O.round_c64(psi) if c64 else psi)
+    got = P.apply_dirac(P.DiracParams(m0=0.1), P.GaugeField(geom, links), P.CloverField(geom, O.pack_clover(cl)),
+                        host_field(psi, 2, geom), dtype=dtype).ksi()
+    assert rel(got, ref) < tol
+
+
+@pytest.mark.parametrize("dims", [(4, 4, 4, 16), (4, 2, 2, 32)])
+@pytest.mark.parametrize("b,dtype,tol", [(4, "c128", 1e-12), (12, "c128", 1e-12), (8, "c64", 1e-5)])
+def test_schur_clover_wide_rhs_matches_oracle(dims, b, dtype, tol):
+    """Both clover modes at nrhs >= 4: M = D_oo^-1 on the eliminated hop,
+    -C_ee x on the kept one."""
+    geom = P.LatticeGeometry(dims)
+    links = O.flip_time_boundary(O.near_unit_gauge(dims, 0.3, 24), dims)
+    cl = O.gen_clover_random(dims, 0.1, 25)
+    v = O.gen_spinor(geom.n_sites // 2, b, 26)
+    c64 = dtype == "c64"
+    from paper_2601_05816_b200.device import upload
+    for keep in (0, 1):
+        so = O.SchurOracle(dims, 0.1, O.round_c64(links) if c64 else links, O.round_c64(cl) if c64 else cl,
+                           keep_parity=keep)
+        ref = so.apply(O.round_c64(v) if c64 else v)
+        sp = P.SchurOperator(P.DiracParams(m0=0.1), P.GaugeField(geom, links),
+                             P.CloverField(geom, O.pack_clover(cl)), keep_parity=keep, dtype=dtype)
+        got = sp.apply_device(upload(host_field(v, 2), dtype, parity=keep)).logical()
+        assert rel(got, ref) < tol
+
+
 @pytest.mark.parametrize("dims", [(4, 4, 4, 16), (4, 2, 2, 32), (6, 2, 4, 16), (4, 2, 2, 48)])
 @pytest.mark.parametrize("b,dtype,tol", [(4, "c128", 1e-12), (12, "c128", 1e-12), (16, "c128", 1e-12),
                                          (8, "c64", 1e-5), (16, "c64", 1e-5)])

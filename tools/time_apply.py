@@ -29,6 +29,7 @@ ap.add_argument("--dtypes", nargs="+", default=["c128", "c64"])
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--parity", type=int, default=-1, help="destination parity of a checkerboard hop (-1: full)")
 ap.add_argument("--cold", action="store_true", help="time each launch alone after an L2 flush (512 MB memset)")
+ap.add_argument("--clover", type=int, default=0, help="clover mode of the hop (1: -C x, 2: M(...)); random blocks")
 ap.add_argument("--idle", type=float, default=0.0, help="with --cold: seconds the GPU idles before each launch")
 a = ap.parse_args()
 pk = ROOT / "MEASURED_PEAKS.json"
@@ -42,6 +43,8 @@ for dt in a.dtypes:
     w = 16 if dt == "c128" else 8
     code = 0 if dt == "c128" else 1
     U = torch.randn((4 * (n // 8) * 72,), dtype=tdt, device="cuda")
+    # packed 2 x 21 Hermitian blocks per destination site, 8-site blocked (layout.cuh clover_base)
+    CL = torch.randn((((n if a.parity < 0 else n // 2) // 8) * 336,), dtype=tdt, device="cuda") if a.clover else None
     for b in a.b:
         nf = n if a.parity < 0 else n // 2
         fb = nf * 12 * b * w
@@ -51,6 +54,11 @@ for dt in a.dtypes:
 
         def go(i):
             x = ps[i % nbuf]
+            if a.clover:
+                _lib.call("b200wd_hop_clover", lat, code, b, a.parity, U.data_ptr(), x.data_ptr(), x.data_ptr(),
+                          es[i % nbuf].data_ptr(), 4.1, -1.0, None, 0, T, None, None, CL.data_ptr(), a.clover,
+                          None)
+                return
             _lib.call("b200wd_hop", lat, code, b, a.parity, U.data_ptr(), x.data_ptr(),
                       x.data_ptr() if a.parity < 0 else None,
                       es[i % nbuf].data_ptr(), 4.1, -1.0, None, 0, T, None, None, None)
@@ -84,7 +92,9 @@ for dt in a.dtypes:
             torch.cuda.synchronize()
             t = e0.elapsed_time(e1) / a.iters * 1e-3
         alg = (24 * b + 36) * w * n if a.parity < 0 else (24 * b + 72) * w * nf  # parity: half fields, all links
-        print(f"{dt} dims={a.dims} par={a.parity} b={b:3d} {t*1e3:8.4f} ms  {nf*b/t:10.3e} site*rhs/s  {alg/t/1e9:8.1f} GB/s  "
+        if a.clover:
+            alg += 42 * w * nf + (12 * b * w * nf if a.parity >= 0 else 0)  # clover blocks (+ xself of a parity hop)
+        print(f"{dt} dims={a.dims} par={a.parity} clov={a.clover} b={b:3d} {t*1e3:8.4f} ms  {nf*b/t:10.3e} site*rhs/s  {alg/t/1e9:8.1f} GB/s  "
               f"frac {alg/t/1e9/peak:.3f}", flush=True)
         del ps, es
         torch.cuda.empty_cache()
