@@ -108,6 +108,50 @@ class ClockSampler:
 # ---- GPU arm ------------------------------------------------------------------
 
 
+def gpu_clover(args, torch, P, nrhs=(4, 12, 16)):
+    """Clover D_W apply (the reference CLI's default clover.mode
+    is random) on configs[1]'s lattice: random clover (scale 0.1), both dtypes,
+    rotating buffers.  Compulsory bytes add the packed blocks: (24 b + 36 + 42) w."""
+    from paper_2601_05816_b200.device import DeviceField
+    dev = torch.device("cuda", 0)
+    geom = P.LatticeGeometry(CFG2_DIMS)
+    n = geom.n_sites
+    gauge = P.gen_gauge(geom, "random", seed=0)
+    clover = P.gen_clover(geom, "random", scale=0.1, seed=1)
+    from paper_2601_05816_b200 import _lib
+    _, l2 = _l2_bytes(_lib)
+    hbm_peak, _ = peaks()
+    out = []
+    for dt in ("c128", "c64"):
+        w = 16 if dt == "c128" else 8
+        op = P.DiracOperator(P.DiracParams(m0=M0), gauge, clover, dt)
+        tdt = torch.complex128 if dt == "c128" else torch.complex64
+        for b in nrhs:
+            nbuf = max(2, int(np.ceil(4 * l2 / (2 * n * 12 * b * w))) + 1)
+            g = torch.Generator(device="cpu").manual_seed(100 + b)
+            base = torch.randn((n // 8, 12, 8, b), dtype=torch.complex128, generator=g).to(dev, tdt)
+            psis = [DeviceField(base.clone(), n, geom) for _ in range(nbuf)]
+            etas = [p_.empty_like() for p_ in psis]
+            for i in range(max(3, args.warmup)):
+                op.apply_device(psis[i % nbuf], etas[i % nbuf])
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for i in range(args.steps):
+                op.apply_device(psis[i % nbuf], etas[i % nbuf])
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) * 1e-3 / args.steps
+            alg = (24 * b + 36 + 42) * w * n
+            out.append({"dtype": dt, "nrhs": b, "ms": round(t * 1e3, 4), "site_rhs_per_s": n * b / t,
+                        "hbm_gbs": round(alg / t / 1e9, 1), "frac": round(alg / t / 1e9 / hbm_peak, 4),
+                        "kernel": "hop_kernel (generic, clover epilogue)"})
+            del psis, etas, base
+        del op
+    torch.cuda.empty_cache()
+    return {"lattice": list(CFG2_DIMS), "clover": "random, scale 0.1", "records": out}
+
+
 def gpu_sweep(args, torch, P):
     from paper_2601_05816_b200 import _lib
     from paper_2601_05816_b200.device import DeviceField, upload_gauge
@@ -464,6 +508,7 @@ def main():
         "e2e": e2e, "gpu_launches": args.steps, "clocks": clk,
         "sweep": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()} for r in sweep],
     }
+    line["clover"] = gpu_clover(args, torch, P)
     if not args.no_gmres:
         line["gmres"] = gpu_gmres(args, torch, P)
         line["gmres"]["cpu_compare"] = gmres_cpu_compare(torch, P, not args.no_cpu)

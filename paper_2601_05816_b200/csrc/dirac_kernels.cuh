@@ -355,7 +355,14 @@ __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, cons
 #else
 #define B200WD_RING_BOUNDS(...) __launch_bounds__(__VA_ARGS__)
 #endif
-template <typename R, int V, int B, int NB, bool PAR, bool TILED, bool ZG>
+// CLOV: site-local 12x12 block term (p.clov_mode 1: - C x; 2: M (alpha x +
+// beta H)) in the epilogue, the generic kernel's algebra.  The producer stages
+// each item's packed blocks in a double-buffered shared-memory area behind the
+// ring (kClovBufs buffers with their own full/empty barriers).
+constexpr int kClovBufs = 2;
+template <typename R, int NB> __host__ __device__ constexpr int clov_tile() { return NB * 336; }
+
+template <typename R, int V, int B, int NB, bool PAR, bool TILED, bool ZG, bool CLOV = false>
 __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_kernel(const HopParams p,
                                                                                    int64_t n_items, int S) {
   using C = cx<R>;
@@ -365,14 +372,23 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
   if (hop_stopped(p)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   C* ring = reinterpret_cast<C*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + S * Sh::SLOT);
+  C* cbuf = ring + S * Sh::SLOT;  // CLOV: kClovBufs block tiles
+  uint64_t* full = reinterpret_cast<uint64_t*>(cbuf + (CLOV ? kClovBufs * clov_tile<R, NB>() : 0));
   uint64_t* empty = full + S;
+  uint64_t* cfull = empty + S;
+  uint64_t* cempty = cfull + kClovBufs;
 
   const int tid = threadIdx.x;  // 1-D block: consumers [0, NC), producer warp [NC, NC+32)
   if (tid == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], Sh::NCW);
+    }
+    if constexpr (CLOV) {
+      for (int i = 0; i < kClovBufs; ++i) {
+        mbar_init(&cfull[i], 1);
+        mbar_init(&cempty[i], Sh::NCW);
+      }
     }
     fence_barrier_init();
   }
@@ -386,6 +402,8 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
       // after a whole T slice (natural order: no reuse to protect)
       const uint64_t pol_t1 = p.hint_t1 == 2 ? l2_evict_last_policy() : pol_first;
       uint32_t pphase = 0;  // phase of the next fill of pslot; its release is phase^1 of empty
+      int cb_slot = 0, cb_first = 1;
+      uint32_t cb_phase = 0;
       const uint32_t lz = (uint32_t)(p.Z / (8 * F * NB));
       for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int64_t gb0 = (p.d_begin >> 3) + (TILED ? item_nat(it, p, lz) : it) * NB;
@@ -418,6 +436,18 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
     }                                                                                       \
   }
         B200WD_PRODUCE(6)
+        if constexpr (CLOV) {  // this item's blocks (read in the epilogue)
+          if (cb_first == 0) mbar_wait(&cempty[cb_slot], cb_phase ^ 1u);
+          constexpr uint32_t cbytes = (uint32_t)(clov_tile<R, NB>() * sizeof(C));
+          mbar_expect_tx(&cfull[cb_slot], cbytes);
+          bulk_g2s(cbuf + cb_slot * clov_tile<R, NB>(), static_cast<const C*>(p.clov) + gb0 * 336, cbytes,
+                   &cfull[cb_slot]);
+          if (++cb_slot == kClovBufs) {
+            cb_slot = 0;
+            cb_phase ^= 1u;
+            cb_first = 0;
+          }
+        }
         B200WD_PRODUCE(0)
         B200WD_PRODUCE(1)
         B200WD_PRODUCE(2)
@@ -448,6 +478,8 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
 
   int cslot = 0;
   uint32_t cphase = 0;
+  int kslot = 0;
+  uint32_t kphase = 0;
   const uint32_t lz = (uint32_t)(p.Z / (8 * F * NB));
   for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
     // natural order keeps gb0 affine in `it`: a separate instantiation,
@@ -565,12 +597,66 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
 #undef B200WD_CONSUME
 
     C* out = static_cast<C*>(p.out) + spinor_base(d, 12, B) + r0;
+    if constexpr (CLOV) {
+      // beta acc = alpha x + beta H; mode 1: s (beta acc - C x), mode 2: s M (beta acc).
+      // One 6x6 block at a time, its elements read from shared memory as used
+      // (volatile: not hoisted into registers).
+      const C* xs = p.xself ? static_cast<const C*>(p.xself) + spinor_base(d, 12, B) + r0 : nullptr;
+      mbar_wait(&cfull[kslot], kphase);
+      const volatile C* cl = cbuf + kslot * clov_tile<R, NB>() + j * 336 + lo;
+      const R beta = R(p.beta);
+      const bool m1 = p.clov_mode == 1;
 #pragma unroll
-    for (int k = 0; k < 12; ++k) {
-      C res[V];
+      for (int v = 0; v < V; ++v) {
+        const R sc = p.scale ? R(__ldg(p.scale + r0 + v)) : R(1);
 #pragma unroll
-      for (int v = 0; v < V; ++v) res[v] = mk(scb[v] * acc[v][k].x, scb[v] * acc[v][k].y);
-      VecIO<R, V>::st(out + k * KST, res);
+        for (int q = 0; q < 2; ++q) {
+          C in[6];  // mode 1: x; mode 2: beta acc
+#pragma unroll
+          for (int k = 0; k < 6; ++k) {
+            if (m1) {
+              C t[V];
+              if (xs) VecIO<R, V>::ld(t, xs + (6 * q + k) * KST);
+              in[k] = xs ? t[v] : mk(R(0), R(0));
+            } else {
+              in[k] = mk(beta * acc[v][6 * q + k].x, beta * acc[v][6 * q + k].y);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 6; ++i) {
+            C y = mk(R(0), R(0));
+#pragma unroll
+            for (int jj = 0; jj < 6; ++jj) {
+              const volatile C& e = cl[(q * 21 + (i >= jj ? i * (i + 1) / 2 + jj : jj * (jj + 1) / 2 + i)) * 8];
+              const R ex = e.x, ey = i >= jj ? e.y : -e.y;
+              y = mk(y.x + ex * in[jj].x - ey * in[jj].y, y.y + ex * in[jj].y + ey * in[jj].x);
+            }
+            const C a = acc[v][6 * q + i];
+            acc[v][6 * q + i] = m1 ? mk(sc * (beta * a.x - y.x), sc * (beta * a.y - y.y)) : mk(sc * y.x, sc * y.y);
+          }
+        }
+      }
+      __syncwarp();
+      if (lead) mbar_arrive(&cempty[kslot]);
+      if (++kslot == kClovBufs) {
+        kslot = 0;
+        kphase ^= 1u;
+      }
+#pragma unroll
+      for (int k = 0; k < 12; ++k) {
+        C res[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) res[v] = acc[v][k];
+        VecIO<R, V>::st(out + k * KST, res);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 12; ++k) {
+        C res[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) res[v] = mk(scb[v] * acc[v][k].x, scb[v] * acc[v][k].y);
+        VecIO<R, V>::st(out + k * KST, res);
+      }
     }
   }
 }
@@ -651,12 +737,12 @@ static void choose_tiles(HopParams& p, int F, int NB, size_t bytes_per_field_sit
 template <int NB>
 static int64_t n_items_of(int64_t nblk) { return nblk / NB; }
 
-template <typename R, int V, int B, int NB, bool PAR, bool TILED, bool ZG>
+template <typename R, int V, int B, int NB, bool PAR, bool TILED, bool ZG, bool CLOV = false>
 static bool launch_ring_kernel(const HopParams& p, int64_t n_items, int S, size_t smem, cudaStream_t st) {
   using Sh = RingShape<R, V, B, NB, PAR>;
   static size_t attr_smem = 0;
   if (attr_smem < smem) {
-    if (cudaFuncSetAttribute(hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG, CLOV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
       return false;
     attr_smem = smem;
@@ -664,7 +750,7 @@ static bool launch_ring_kernel(const HopParams& p, int64_t n_items, int S, size_
   static int occ[9] = {0};  // CTAs per SM by ring depth, queried once
   if (occ[S] == 0) {
     int c = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG>, Sh::NT,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG, CLOV>, Sh::NT,
                                                       smem) !=
             cudaSuccess ||
         c <= 0)
@@ -679,7 +765,7 @@ static bool launch_ring_kernel(const HopParams& p, int64_t n_items, int S, size_
   }
   int64_t grid = (int64_t)occ[S] * sm_count;
   if (grid > n_items) grid = n_items;
-  hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG><<<(unsigned)grid, Sh::NT, smem, st>>>(p, n_items, S);
+  hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG, CLOV><<<(unsigned)grid, Sh::NT, smem, st>>>(p, n_items, S);
   return true;
 }
 
@@ -696,7 +782,8 @@ static bool launch_ring_nb(const HopParams& p_in, int64_t nblk, int S, cudaStrea
     // hops of 32^3 x 64 (tools/variants_cmp.sh); for the full-lattice apply on
     // 48^3 x 96 every patch shape tried (1..8 x 48, 48 x 2..8, 6 x 12) was
     // 10-25% slower than the natural order
-    if (PAR) choose_tiles(p, Sh::F, NB, site_bytes);
+    const bool clov = p.clov_mode != 0;
+    if (PAR && !clov) choose_tiles(p, Sh::F, NB, site_bytes);
     const int64_t slice_bytes = (int64_t)(p.per_t / Sh::F) * (int64_t)site_bytes;
     static const int hints = ring_knob("B200WD_L2HINT", 1);  // read once per process
     p.hint_t1 = hints ? (p.tile_x ? 2 : (slice_bytes > kSliceNoReuse ? 1 : 0)) : 0;
@@ -708,6 +795,18 @@ static bool launch_ring_nb(const HopParams& p_in, int64_t nblk, int S, cudaStrea
     size_t smem = Sh::smem(S);
     while (smem > 227 * 1024 && S > 2) smem = Sh::smem(--S);
     const int64_t ni = n_items_of<NB>(nblk);
+    if (clov) {  // staged blocks take ring slots' place in the same shared-memory budget; natural order
+      if constexpr (sizeof(R) == 8) {  // complex64: the generic kernel is faster (tuning log)
+        const size_t cextra = kClovBufs * (clov_tile<R, NB>() * sizeof(cx<R>) + 16);
+        const size_t budget = smem;
+        while (Sh::smem(S) + cextra > budget && S > 2) --S;
+        smem = Sh::smem(S) + cextra;
+        if (smem > 227 * 1024) return false;
+        if (whole_lines) return launch_ring_kernel<R, V, B, NB, PAR, false, false, true>(p, ni, S, smem, st);
+        return launch_ring_kernel<R, V, B, NB, PAR, false, true, true>(p, ni, S, smem, st);
+      }
+      return false;
+    }
     if constexpr (PAR) {
       if (p.tile_x) {
         if (whole_lines) return launch_ring_kernel<R, V, B, NB, PAR, true, false>(p, ni, S, smem, st);
@@ -782,12 +881,17 @@ static bool try_launch_ring_par(const HopParams& p, int64_t nblk, RingCfg c, cud
   return launch_ring_nb<R, V, B, 1, PAR>(p, nblk, 0, st);
 }
 
-// Launch the ring kernel when its shape preconditions hold (no halos, no
-// clover; full lattice: Z % 8 == 0; checkerboard fields: Z % 16 == 0); false
-// -> the caller uses the generic kernel.
+// Launch the ring kernel when its shape preconditions hold (no halos; full
+// lattice: Z % 8 == 0; checkerboard fields: Z % 16 == 0); false -> the caller
+// uses the generic kernel.  Clover hops take the ring in complex128 except
+// the checkerboard -C x hop with a separate xself (measured slower there);
+// B200WD_RING_CLOVER=0 keeps every clover hop generic.
 template <typename R, int V, int B>
 static bool try_launch_ring(const HopParams& p, cudaStream_t st) {
-  if (p.lam_halo != nullptr || p.beta == 0.0 || p.clov_mode != 0) return false;
+  static const int ring_clover = ring_knob("B200WD_RING_CLOVER", 1);
+  if (p.lam_halo != nullptr || p.beta == 0.0) return false;
+  if (p.clov_mode != 0 && (!ring_clover || sizeof(R) != 8 || (p.dst_parity >= 0 && p.clov_mode == 1)))
+    return false;
   const bool par = p.dst_parity >= 0;
   if (p.Z % (par ? 16 : 8) != 0) return false;
   if ((p.d_begin & 7) || (p.d_end & 7)) return false;

@@ -61,13 +61,13 @@ __device__ __forceinline__ bool hop_stopped(const HopParams& p) {
 
 // y = M t for the two packed Hermitian 6x6 blocks of one site (fields.py:212-247:
 // lower triangle, row-major, element (i,j), i >= j, at i(i+1)/2 + j)
-template <typename C>
+template <bool GLOBAL = true, typename C>
 __device__ __forceinline__ void clover_mul(C (&y)[12], const C (&t)[12], const C* __restrict__ cl) {
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     C a[21];
 #pragma unroll
-    for (int e = 0; e < 21; ++e) a[e] = __ldg(cl + (q * 21 + e) * 8);
+    for (int e = 0; e < 21; ++e) a[e] = GLOBAL ? __ldg(cl + (q * 21 + e) * 8) : cl[(q * 21 + e) * 8];
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
       C acc = mk(decltype(t[0].x)(0), decltype(t[0].x)(0));
