@@ -145,7 +145,8 @@ def gpu_clover(args, torch, P, nrhs=(4, 12, 16)):
             alg = (24 * b + 36 + 42) * w * n
             out.append({"dtype": dt, "nrhs": b, "ms": round(t * 1e3, 4), "site_rhs_per_s": n * b / t,
                         "hbm_gbs": round(alg / t / 1e9, 1), "frac": round(alg / t / 1e9 / hbm_peak, 4),
-                        "kernel": "hop_kernel (generic, clover epilogue)"})
+                        "kernel": ("hop_ring_kernel (blocks staged in shared memory)" if dt == "c128"
+                                   else "hop_kernel (generic, clover epilogue)")})
             del psis, etas, base
         del op
     torch.cuda.empty_cache()
