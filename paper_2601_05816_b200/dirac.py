@@ -108,13 +108,6 @@ def clover_is_zero(clover) -> bool:
     return clover is None or (clover.is_zero() if hasattr(clover, "is_zero") else not np.any(clover.data))
 
 
-def _check_clover(clover) -> None:
-    """Paths that implement C = 0 only (the multi-GPU T split) reject a clover term."""
-    if not clover_is_zero(clover):
-        raise NotImplementedError("this path implements C = 0 (the BASELINE multi-GPU configurations); "
-                                  "use the single-GPU operators for a non-zero clover term")
-
-
 class DiracOperator:
     """D = (4+m0) - H on the full (single-GPU) lattice, device resident.
 

@@ -119,6 +119,7 @@ class SchurOperator:
         # condition number 1, or infinite when 4+m0 = 0 (oddeven.py:123-132)
         self.diag = 4.0 + params.m0
         self.clover_inv = self.clover_keep = None
+        # local parity == global parity: slab extents and T origins are even (dirac.cu fill_params)
         elim = self.geom.odd_sites if keep_parity == 0 else self.geom.even_sites
         if clover_is_zero(clover):
             if self.diag == 0.0 or not np.isfinite(self.diag):
@@ -152,9 +153,7 @@ class SchurOperator:
     # -- device kernels ----------------------------------------------------------
     def _hop(self, dst_parity, src, out, xself, alpha, beta, scale=None, clover=None, mode=0):
         if self.comm is not None:
-            if clover is not None:
-                raise NotImplementedError("the T split implements C = 0")
-            self.comm.hop(dst_parity, src, out, xself, alpha, beta, scale)
+            self.comm.hop(dst_parity, src, out, xself, alpha, beta, scale, clover=clover, mode=mode)
         else:
             hop_device(self.lat, self.dtype, src.b, dst_parity, self.gauge, src, out, xself, alpha, beta, scale,
                        clover=clover, clover_mode=mode)

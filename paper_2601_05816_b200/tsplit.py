@@ -17,6 +17,10 @@ Per operator apply (halo.py:339-387 semantics, on the device):
 4. after the receives complete, the two boundary slices consume the halos
    (``b200wd_hop`` with ``lam_halo``/``chi_halo``).
 
+A clover term (this rank's slab of packed blocks, uploaded once in ``bind``)
+rides in the epilogue of every interior and boundary hop (``b200wd_hop_clover``),
+so the full apply and the distributed Schur operator take it too.
+
 GMRES reductions are one ``all_reduce`` of the b partial sums per reducing pass.
 With one rank the split degenerates to the single-GPU periodic apply.
 The antiperiodic time boundary rides in the links of the rank that owns global
@@ -27,6 +31,7 @@ from __future__ import annotations
 
 import time
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -47,7 +52,13 @@ class CudaHaloKernels:
         _lib.call("b200wd_halo_pack", lat, dtype_code(dtype), b, src_parity, gauge.ptr, src.ptr, ptr(lam), ptr(chi),
                   stream_ptr())
 
-    def hop(self, lat, dtype, b, dst_parity, gauge, src, out, xself, alpha, beta, scale, t0, t1, lam=None, chi=None):
+    def hop(self, lat, dtype, b, dst_parity, gauge, src, out, xself, alpha, beta, scale, t0, t1, lam=None, chi=None,
+            clover=None, mode=0):
+        if clover is not None:  # site-local block term in the epilogue (mode 1: -C x, 2: M (...))
+            _lib.call("b200wd_hop_clover", lat, dtype_code(dtype), b, dst_parity, gauge.ptr, src.ptr,
+                      None if xself is None else xself.ptr, out.ptr, float(alpha), float(beta), ptr(scale), int(t0),
+                      int(t1), ptr(lam), ptr(chi), clover.ptr, int(mode), stream_ptr())
+            return
         _lib.call("b200wd_hop", lat, dtype_code(dtype), b, dst_parity, gauge.ptr, src.ptr,
                   None if xself is None else xself.ptr, out.ptr, float(alpha), float(beta), ptr(scale), int(t0),
                   int(t1), ptr(lam), ptr(chi), stream_ptr())
@@ -113,47 +124,62 @@ class TSplitComm:
         return dist.batch_isend_irecv(ops)
 
     # -- the split hop ----------------------------------------------------------
-    def hop(self, dst_parity, src, out, xself, alpha, beta, scale=None, gauge=None):
+    def hop(self, dst_parity, src, out, xself, alpha, beta, scale=None, gauge=None, clover=None, mode=0):
         """out = scale (alpha xself + beta H src) on the local slab with halos.
 
         ``dst_parity`` None/-1 for full fields, else the parity of ``out``
-        (``src`` has the other parity)."""
+        (``src`` has the other parity).  ``clover`` (device packed blocks of the
+        destination sites) with ``mode`` 1 subtracts C xself, mode 2 applies the
+        blocks to the whole result (the Schur D_ee^-1 hop)."""
         gauge = gauge if gauge is not None else self.gauge
         par = -1 if dst_parity is None else dst_parity
         b, dtype = src.b, src.dtype
         T = self.local_geom.dims[0]
         k = self.kernels
+        extra = {} if clover is None else {"clover": clover, "mode": mode}
         if self.world == 1:
-            k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 0, T)
+            k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 0, T, **extra)
             return out
         f = self._face_buffers(None if par < 0 else 1 - par, b, dtype, src.data.device)
         k.pack(self.lat, dtype, b, -1 if par < 0 else 1 - par, gauge, src, f["lam"], f["chi"])
         reqs = self.exchange(f["lam"], f["chi"], f["lam_in"], f["chi_in"])
         if T > 2:
-            k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 1, T - 1)
+            k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 1, T - 1, **extra)
         for r in reqs:
             r.wait()
-        k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 0, 1, f["lam_in"], f["chi_in"])
+        k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 0, 1, f["lam_in"], f["chi_in"],
+              **extra)
         k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, T - 1, T, f["lam_in"],
-              f["chi_in"])
+              f["chi_in"], **extra)
         self.stats["applies"] += 1
         return out
 
     # -- reference comm protocol ----------------------------------------------------
     def bind(self, params, gauge, clover=None, dtype="c128"):
-        """Attach the local links (this rank's slab) and mass; returns self."""
-        from .dirac import _check_clover
-        _check_clover(clover)
+        """Attach the local links and clover (this rank's slab) and mass; returns self."""
+        from .dirac import clover_is_zero
         if gauge.geom.dims != self.local_geom.dims:
             raise ValueError(f"gauge slab {gauge.geom.dims} != local geometry {self.local_geom.dims}")
         self.params = params
         self.dtype = dtype
         self.gauge = gauge_cache.get(gauge, dtype)
+        if clover_is_zero(clover):
+            self.clover = None
+        else:
+            if clover.geom.dims != self.local_geom.dims:
+                raise ValueError(f"clover slab {clover.geom.dims} != local geometry {self.local_geom.dims}")
+            key = (id(clover.data), dtype)
+            if getattr(self, "_clover_key", None) != key:  # uploaded once per field and precision
+                from .device import upload_packed_blocks
+                self._clover_dev = upload_packed_blocks(np.asarray(clover.data), dtype)
+                self._clover_key = key
+            self.clover = self._clover_dev
         return self
 
     def apply_device(self, v: DeviceField, out: DeviceField | None = None, scale=None) -> DeviceField:
         out = v.empty_like() if out is None else out
-        return self.hop(None, v, out, v, 4.0 + self.params.m0, -1.0, scale)
+        return self.hop(None, v, out, v, 4.0 + self.params.m0, -1.0, scale, clover=self.clover,
+                        mode=0 if self.clover is None else 1)
 
     def __call__(self, v):
         if isinstance(v, DeviceField):
@@ -192,8 +218,6 @@ class TSplitComm:
 
     def solve_dirac(self, params, gauge, clover, eta, cfg, odd_even=False, psi0=None):
         """gmres.py:353-385 on the split lattice (eta: this rank's slab)."""
-        import numpy as np
-
         from .blas import block_norm2_device
         from .gmres import SolveReport, _sub, gmres_solve
         from .oddeven import device_split

@@ -172,22 +172,25 @@ def test_gmres_matches_oracle_dirac_small():
     assert np.abs(res.psi.ksi() - ref.psi).max() / np.abs(ref.psi).max() < 1e-8
 
 
-def test_tsplit_comm_single_rank_matches_single_gpu():
-    """TSplitComm with one rank (no process group) is the single-GPU path."""
+@pytest.mark.parametrize("with_clover", [False, True])
+def test_tsplit_comm_single_rank_matches_single_gpu(with_clover):
+    """TSplitComm with one rank (no process group) is the single-GPU path,
+    with and without a clover term."""
     from paper_2601_05816_b200.tsplit import TSplitComm
     dims = (8, 4, 4, 4)
     geom = P.LatticeGeometry(dims)
     links = O.flip_time_boundary(O.near_unit_gauge(dims, 0.3, 11), dims)
     gauge = P.GaugeField(geom, links)
+    clover = P.CloverField(geom, O.pack_clover(O.gen_clover_random(dims, 0.05, 3))) if with_clover else None
     eta = host_field(O.gen_spinor(512, 4, 13), 2, geom)
     comm = TSplitComm(geom)
-    d1 = P.apply_dirac(P.DiracParams(m0=0.1), gauge, None, eta, comm=comm).ksi()
-    d0 = P.apply_dirac(P.DiracParams(m0=0.1), gauge, None, eta).ksi()
+    d1 = P.apply_dirac(P.DiracParams(m0=0.1), gauge, clover, eta, comm=comm).ksi()
+    d0 = P.apply_dirac(P.DiracParams(m0=0.1), gauge, clover, eta).ksi()
     assert np.abs(d1 - d0).max() == 0.0
     cfg = P.GmresConfig(restart_len=30, restarts=20, tol=1e-10)
     for oe in (False, True):
-        r1 = P.solve_dirac(P.DiracParams(m0=0.1), gauge, None, eta, cfg, odd_even=oe, comm=comm)
-        r0 = P.solve_dirac(P.DiracParams(m0=0.1), gauge, None, eta, cfg, odd_even=oe)
+        r1 = P.solve_dirac(P.DiracParams(m0=0.1), gauge, clover, eta, cfg, odd_even=oe, comm=comm)
+        r0 = P.solve_dirac(P.DiracParams(m0=0.1), gauge, clover, eta, cfg, odd_even=oe)
         assert r1.iterations == r0.iterations
         assert np.all(r1.full_relnorms <= 1e-10)
 

@@ -50,9 +50,11 @@ class OracleHaloKernels:
         lam.copy_(torch.from_numpy(2 * lam_down.reshape(self.per_t, 6, -1)))
         chi.copy_(torch.from_numpy(2 * chi_up.reshape(self.per_t, 6, -1)))
 
-    def hop(self, lat, dtype, b, dst_parity, gauge, src, out, xself, alpha, beta, scale, t0, t1, lam=None, chi=None):
+    def hop(self, lat, dtype, b, dst_parity, gauge, src, out, xself, alpha, beta, scale, t0, t1, lam=None, chi=None,
+            clover=None, mode=0):
         assert dst_parity == -1 and xself is src and beta == -1.0
         assert abs(alpha - (4.0 + M0)) < 1e-15
+        assert (clover is None) == (mode == 0) and mode in (0, 1)
         psi = src.data.numpy()
         if lam is None:
             res = O.apply_dirac(self.ldims, M0, self.links, None, psi)
@@ -60,6 +62,9 @@ class OracleHaloKernels:
             lh = (lam.numpy() / 2).reshape(self.per_t, 2, 3, -1)
             ch = (chi.numpy() / 2).reshape(self.per_t, 2, 3, -1)
             res = O.tsplit_local_apply(self.ldims, M0, self.links, psi, lh, ch)
+        if clover is not None:  # mode 1: - C x, site-local
+            res = res + (O.apply_dirac(self.ldims, M0, self.links, clover, psi)
+                         - O.apply_dirac(self.ldims, M0, self.links, None, psi))
         sl = slice(t0 * self.per_t, t1 * self.per_t)
         out.data[sl] = torch.from_numpy(res[sl])
 
@@ -70,7 +75,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, with_clover=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -88,8 +93,12 @@ def _worker(rank, world, port, q):
         comm = TSplitComm(geom, kernels=kern)
         src = _Field(psi[sl])
         out = _Field(np.zeros_like(psi[sl]))
-        comm.hop(None, src, out, src, 4.0 + M0, -1.0, gauge=object())
-        full = O.apply_dirac(DIMS, M0, links, None, psi)
+        cl = O.gen_clover_random(DIMS, 0.1, 7) if with_clover else None
+        if with_clover:  # the clover slab rides with every interior and boundary hop
+            comm.hop(None, src, out, src, 4.0 + M0, -1.0, gauge=object(), clover=cl[sl], mode=1)
+        else:
+            comm.hop(None, src, out, src, 4.0 + M0, -1.0, gauge=object())
+        full = O.apply_dirac(DIMS, M0, links, cl, psi)
         err = float(np.abs(out.data.numpy() - full[sl]).max() / np.abs(full).max())
         # all-reduce of per-rank partial dots == global dot
         part = torch.from_numpy(np.einsum("xkb,xkb->b", psi[sl].conj(), full[sl]))
@@ -101,12 +110,12 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [1, 2, 4])
-def test_tsplit_host_logic_gloo(world):
+@pytest.mark.parametrize("world,with_clover", [(1, False), (2, False), (4, False), (2, True)])
+def test_tsplit_host_logic_gloo(world, with_clover):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, with_clover)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in range(world)]
