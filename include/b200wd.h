@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define B200WD_ABI_VERSION 2
+#define B200WD_ABI_VERSION 3
 
 #define B200WD_OK 0
 #define B200WD_ERR_ARG 1         /* bad shape / layout / parameter -> ValueError      */
@@ -182,7 +182,23 @@ typedef struct b200wd_gmres_state {
   void* dot;             /* complex128 [b]  result of the last reducing pass    */
   void* y;               /* complex128 [b][m] least-squares solution            */
   void* scratch;         /* b200wd_reduce_scratch_bytes(b) bytes                */
+  /* B200 extension (not in the reference): Gram-Schmidt variant of the
+   * library-issued Arnoldi step.  B200WD_ORTH_MGS (0, zero-initialised
+   * default) is the reference's modified Gram-Schmidt (gmres.py:118-121);
+   * B200WD_ORTH_CGS (1) is classical Gram-Schmidt: all j+1 projections in one
+   * pass over the basis, then one update pass that also forms ||w||^2 -- about
+   * half the HBM traffic of MGS, orthogonality loss O(eps kappa^2) instead of
+   * O(eps kappa).  CGS needs the cooperative sweep (single rank) and
+   * cgs_partials (b200wd_cgs_scratch_bytes(b, m) bytes). */
+  int32_t orth;
+  void* cgs_partials;
 } b200wd_gmres_state;
+
+#define B200WD_ORTH_MGS 0
+#define B200WD_ORTH_CGS 1
+
+/* Bytes of b200wd_gmres_state.cgs_partials for b rhs and restart length m. */
+int64_t b200wd_cgs_scratch_bytes(int32_t b, int32_t m);
 
 /* eta_norm := sqrt(dot) (dot = ||eta||^2 from b200wd_block_norm2 into
  * st->dot, all-reduced), breakdown flags cleared (gmres.py:204-205). */

@@ -17,7 +17,7 @@ LIB_PATH = Path(os.environ.get("B200WD_LIB") or Path(__file__).resolve().parent 
 
 OK, ERR_ARG, ERR_CUDA, ERR_SINGULAR, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 C128, C64 = 0, 1
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class B200Unavailable(RuntimeError):
@@ -42,6 +42,7 @@ class GmresState(C.Structure):
         ("h_raw", C.c_void_p), ("h", C.c_void_p), ("gamma", C.c_void_p), ("cs", C.c_void_p),
         ("sn", C.c_void_p), ("sigma", C.c_void_p), ("eta_norm", C.c_void_p), ("relnorm", C.c_void_p),
         ("breakdown", C.c_void_p), ("dot", C.c_void_p), ("y", C.c_void_p), ("scratch", C.c_void_p),
+        ("orth", C.c_int32), ("cgs_partials", C.c_void_p),
     ]
 
 
@@ -109,6 +110,7 @@ SIGNATURES = {
     "b200wd_clover_import": [_vp, _i64, _vp, _i32, _vp],
     "b200wd_halo_pack": [_LAT, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp],
     "b200wd_reduce_scratch_bytes": [_i32],
+    "b200wd_cgs_scratch_bytes": [_i32, _i32],
     "b200wd_block_dot": [_i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp],
     "b200wd_block_norm2": [_i64, _i32, _i32, _vp, _vp, _vp, _vp],
     "b200wd_block_axpy": [_i64, _i32, _i32, _vp, _vp, _vp, _vp],
@@ -124,7 +126,8 @@ SIGNATURES = {
     "b200wd_gmres_arnoldi": [_ST, _OP, _i32, _i64, C.POINTER(_vp), _vp, _vp],
     "b200wd_gmres_cycle": [_ST, _OP, _i32, _i64, C.POINTER(_vp), _dbl, _i32, _vp, _vp, _vp, _vp, _vp],
 }
-RESTYPES = {"b200wd_last_error": C.c_char_p, "b200wd_reduce_scratch_bytes": _i64}
+RESTYPES = {"b200wd_last_error": C.c_char_p, "b200wd_reduce_scratch_bytes": _i64,
+            "b200wd_cgs_scratch_bytes": _i64}
 
 _lib = None
 

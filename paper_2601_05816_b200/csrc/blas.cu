@@ -160,6 +160,7 @@ struct GState {
   double *cs, *sigma, *eta_norm, *relnorm;
   int* brk;
   Scratch sc;
+  double2* cgs;  // [m+1][grid][b] block partials of the CGS projection pass
 };
 
 static GState gstate(const b200wd_gmres_state* st) {
@@ -179,6 +180,7 @@ static GState gstate(const b200wd_gmres_state* st) {
   g.relnorm = static_cast<double*>(st->relnorm);
   g.brk = static_cast<int*>(st->breakdown);
   g.sc = scratch_of(st->scratch, st->b);
+  g.cgs = static_cast<double2*>(st->cgs_partials);
   return g;
 }
 
@@ -492,12 +494,85 @@ __global__ void arnoldi_sweep_kernel(int j, int64_t n, int s, ZList zl, double2*
   }
 }
 
+
+// ---- classical Gram-Schmidt sweep (B200 extension, b200wd_gmres_state.orth) --
+// Pass A: all j+1 projections <Z_p, w> in one pass over the basis (the
+// accumulators of kCgsChunk basis vectors live in registers, so w is re-read
+// once per chunk); block partials per p, block p folds projection p (distributed
+// fold), h_raw[p][j] = sigma_p <Z_p,w> and the update coefficient
+// -sigma_p h_p go to y (free scratch until the cycle's back substitution).
+// Pass B: w -= sum_p c_p Z_p with ||w||^2 formed from the stored result, then
+// the column close.  Traffic (j+1)(2 + 1/kCgsChunk) F + 3F vs 4(j+1)+2 F for MGS.
+constexpr int kCgsChunk = 8;
+
+__global__ void arnoldi_cgs_kernel(int j, int64_t n, int s, ZList zl, double2* w, GState g, const int* stop) {
+  if (stop != nullptr && *static_cast<const volatile int*>(stop) != 0) return;  // cycle already converged
+  extern __shared__ double2 red[];  // [S][b] reduction tree, then [j+1][b] coefficients
+  cg::grid_group grid = cg::this_grid();
+  const int b = blockDim.x, r = threadIdx.x, y = threadIdx.y, S = blockDim.y;
+  const int m = g.m;
+  const int64_t ng = groups(n, s);
+  const int64_t g0 = (int64_t)blockIdx.x * S + y, gst = (int64_t)gridDim.x * S;
+  const size_t pstride = (size_t)gridDim.x * b;
+  for (int p0 = 0; p0 <= j; p0 += kCgsChunk) {
+    const int np = min(kCgsChunk, j + 1 - p0);
+    double2 a[kCgsChunk];
+#pragma unroll
+    for (int k = 0; k < kCgsChunk; ++k) a[k] = make_double2(0.0, 0.0);
+    for (int64_t q = g0; q < ng; q += gst) {
+      const int64_t i = q * b + r;
+      const double2 wv = w[i];
+#pragma unroll
+      for (int k = 0; k < kCgsChunk; ++k)
+        if (k < np) acc_dot(a[k], __ldg(zl.z[p0 + k] + i), wv);
+    }
+#pragma unroll
+    for (int k = 0; k < kCgsChunk; ++k)
+      if (k < np) block_partial(a[k], red, g.cgs + (size_t)(p0 + k) * pstride);
+  }
+  grid.sync();
+  for (int p = blockIdx.x; p <= j; p += gridDim.x) {
+    const double2 d = fold_partials(g.cgs + (size_t)p * pstride, red);
+    if (y == 0) {
+      const double sig = g.sigma[(size_t)p * g.b + r];
+      const double2 hp = make_double2(sig * d.x, sig * d.y);
+      g.h_raw[((size_t)r * (m + 1) + p) * m + j] = hp;
+      g.y[(size_t)r * m + p] = make_double2(-sig * hp.x, -sig * hp.y);
+    }
+  }
+  grid.sync();
+  double2* coef = red + (size_t)S * b;
+  for (int p = y; p <= j; p += S) coef[p * b + r] = __ldcg(g.y + (size_t)r * m + p);
+  __syncthreads();
+  double2 a = make_double2(0.0, 0.0);
+  for (int64_t q = g0; q < ng; q += gst) {
+    const int64_t i = q * b + r;
+    double2 v = w[i];
+#pragma unroll 4
+    for (int p = 0; p <= j; ++p) v = cmac(v, coef[p * b + r], __ldg(zl.z[p] + i));
+    w[i] = v;
+    a.x = fma(v.x, v.x, a.x);
+    a.x = fma(v.y, v.y, a.x);
+  }
+  block_partial(a, red, g.sc.partials);
+  grid.sync();
+  const double2 d = fold_partials(g.sc.partials, red);
+  if (blockIdx.x == 0 && y == 0) {
+    g.dot[r] = d;
+    close_column_body(j, g, r);
+  }
+}
+
 static dim3 red_block(int b) { return dim3(b, rows_per_block(b)); }
 static size_t red_smem(int b) { return (size_t)b * rows_per_block(b) * sizeof(double2); }
 
 }  // namespace b200wd
 
 using namespace b200wd;
+
+extern "C" int64_t b200wd_cgs_scratch_bytes(int32_t b, int32_t m) {
+  return (int64_t)(m + 1) * kMaxGrid * b * (int64_t)sizeof(double2);
+}
 
 extern "C" int64_t b200wd_reduce_scratch_bytes(int32_t b) {
   return 2 * (int64_t)kMaxGrid * b * (int64_t)sizeof(double2) + 64;
@@ -553,9 +628,11 @@ extern "C" int b200wd_block_scale(int64_t n_sites, int32_t s, int32_t b, const v
 
 #define CHECK_STATE(st)                                                                        \
   B200WD_REQUIRE((st) != nullptr && (st)->b >= 1 && (st)->b <= kBlock && (st)->m >= 1 &&      \
-                     (st)->m <= kMaxBasis - 1,                                                 \
-                 "bad GMRES state (b must be in [1,%d], restart length in [1,%d])", kBlock, \
-                 kMaxBasis - 1)
+                     (st)->m <= kMaxBasis - 1 &&                                               \
+                     ((st)->orth == B200WD_ORTH_MGS ||                                         \
+                      ((st)->orth == B200WD_ORTH_CGS && (st)->cgs_partials != nullptr)),       \
+                 "bad GMRES state (b must be in [1,%d], restart length in [1,%d], orth 0 or 1 " \
+                 "with cgs_partials for CGS)", kBlock, kMaxBasis - 1)
 
 extern "C" int b200wd_gmres_residual(const b200wd_gmres_state* st, int64_t n_sites, int32_t s, const void* eta,
                                      void* r, void* stream) {
@@ -647,7 +724,9 @@ static bool sweep_single_launch(const b200wd_gmres_state* st, int j, int64_t n_s
   if (!en) return false;
   const dim3 blk = red_block(st->b);
   const int grid = grid_for_sites(n_sites, blk.y);
-  const size_t smem = red_smem(st->b);
+  const bool cgs = st->orth == B200WD_ORTH_CGS;
+  const size_t smem = cgs ? red_smem(st->b) + (size_t)st->m * st->b * sizeof(double2) : red_smem(st->b);
+  const void* kern = cgs ? (const void*)arnoldi_cgs_kernel : (const void*)arnoldi_sweep_kernel;
   static int sm_count = 0, occ[kBlock + 1] = {0};
   if (sm_count == 0) {
     int dev = 0;
@@ -658,13 +737,22 @@ static bool sweep_single_launch(const b200wd_gmres_state* st, int j, int64_t n_s
     if (!coop) en = 0;
   }
   if (!en) return false;
-  if (occ[st->b] == 0) {
-    int c = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, arnoldi_sweep_kernel, blk.x * blk.y, smem) != cudaSuccess)
-      c = -1;
-    occ[st->b] = c > 0 ? c : -1;
+  int occupancy = 0;
+  if (cgs) {  // smem depends on m: no cache
+    if (smem > 48 * 1024 ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occupancy, arnoldi_cgs_kernel, blk.x * blk.y, smem) !=
+            cudaSuccess)
+      occupancy = -1;
+  } else {
+    if (occ[st->b] == 0) {
+      int c = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, arnoldi_sweep_kernel, blk.x * blk.y, smem) != cudaSuccess)
+        c = -1;
+      occ[st->b] = c > 0 ? c : -1;
+    }
+    occupancy = occ[st->b];
   }
-  if (occ[st->b] < 0 || (int64_t)occ[st->b] * sm_count < grid) return false;
+  if (occupancy <= 0 || (int64_t)occupancy * sm_count < grid) return false;
   ZList zl{};
   for (int p = 0; p <= j + 1; ++p) zl.z[p] = static_cast<const double2*>(z[p]);
   GState g = gstate(st);
@@ -673,8 +761,7 @@ static bool sweep_single_launch(const b200wd_gmres_state* st, int j, int64_t n_s
   double2* wp = static_cast<double2*>(w);
   const int* stop = g_hop_stop;
   void* args[] = {&jj, &nn, &ss, &zl, &wp, &g, &stop};
-  if (cudaLaunchCooperativeKernel((const void*)arnoldi_sweep_kernel, dim3(grid), blk, args, smem,
-                                  as_stream(stream)) == cudaSuccess)
+  if (cudaLaunchCooperativeKernel(kern, dim3(grid), blk, args, smem, as_stream(stream)) == cudaSuccess)
     return true;
   (void)cudaGetLastError();  // not sticky: fall back to the per-pass launches
   return false;
@@ -694,6 +781,10 @@ extern "C" int b200wd_gmres_arnoldi(const b200wd_gmres_state* st, const b200wd_o
   const double* sig = static_cast<const double*>(st->sigma) + (int64_t)j * st->b;
   if (int rc = b200wd_operator_apply(op, st->b, z[j], w, sig, stream)) return rc;
   if (!sweep_single_launch(st, j, n_sites, s, z, w, stream)) {
+    if (st->orth == B200WD_ORTH_CGS) {
+      set_error("b200wd_gmres_arnoldi: classical Gram-Schmidt needs the cooperative sweep (m*b <= 2816, co-resident grid)");
+      return B200WD_ERR_UNSUPPORTED;
+    }
     if (int rc = b200wd_gmres_dot(st, n_sites, s, z[0], w, stream)) return rc;
     for (int p = 0; p <= j; ++p)
       if (int rc = b200wd_gmres_mgs(st, j, p, n_sites, s, w, z[p], p < j ? z[p + 1] : nullptr, stream)) return rc;

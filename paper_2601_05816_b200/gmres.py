@@ -44,7 +44,16 @@ _TINY = 1e-300
 
 @dataclass
 class GmresConfig:
-    """gmres.py:42-56.  ``dot_strategy`` is accepted for compatibility."""
+    """gmres.py:42-56.  ``dot_strategy`` is accepted for compatibility.
+
+    ``orthogonalization`` is a B200 extension (not in the reference):
+    ``"mgs"`` (default) is the reference's modified Gram-Schmidt
+    (gmres.py:118-121); ``"cgs"`` is classical Gram-Schmidt in the
+    library-issued Arnoldi step -- one projection pass over the whole basis
+    and one update pass, about half the HBM traffic per iteration.  Its
+    orthogonality loss grows as eps*kappa^2 instead of eps*kappa, so the
+    iteration count can drift from the reference's on ill-conditioned
+    systems; single rank only, and not combined with ``reorthogonalize``."""
 
     restart_len: int = 10
     restarts: int = 10
@@ -53,8 +62,11 @@ class GmresConfig:
     dot_strategy: str = "deferred"
     reorthogonalize: bool = False
     breakdown_rel: float = 1e-14
+    orthogonalization: str = "mgs"
 
     def __post_init__(self) -> None:
+        if self.orthogonalization not in ("mgs", "cgs"):
+            raise ValueError(f"orthogonalization must be 'mgs' or 'cgs', got {self.orthogonalization!r}")
         if self.restart_len < 1 or self.restarts < 1:
             raise ValueError("restart_len and restarts must be >= 1")
         if not self.tol > 0:
@@ -80,7 +92,7 @@ class GmresResult:
 class _State:
     """Device-resident solver state (b200wd_gmres_state)."""
 
-    def __init__(self, b: int, m: int, brk_rel: float, dev):
+    def __init__(self, b: int, m: int, brk_rel: float, dev, cgs: bool = False):
         c128 = dict(dtype=torch.complex128, device=dev)
         f64 = dict(dtype=torch.float64, device=dev)
         self.h_raw = torch.zeros((b, m + 1, m), **c128)
@@ -102,6 +114,10 @@ class _State:
                         ("relnorm", self.relnorm), ("breakdown", self.brk), ("dot", self.dot), ("y", self.y),
                         ("scratch", self.scratch)):
             setattr(st, name, t.data_ptr())
+        if cgs:
+            nbytes = int(_lib.load().b200wd_cgs_scratch_bytes(b, m))
+            self.cgs_partials = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            st.orth, st.cgs_partials = 1, self.cgs_partials.data_ptr()
         self.st = st
         self.ref = ctypes.byref(st)
 
@@ -178,7 +194,8 @@ def gmres_solve(op, eta, psi0, cfg: GmresConfig) -> GmresResult:
     n, s, b = d_eta.n_sites, d_eta.s, d_eta.b
     m = cfg.restart_len
     stream = stream_ptr()
-    st = _State(b, m, cfg.breakdown_rel, dev)
+    cgs = cfg.orthogonalization == "cgs"
+    st = _State(b, m, cfg.breakdown_rel, dev, cgs=cgs)
     L = _lib.load()
 
     def chk(rc, name):
@@ -200,6 +217,9 @@ def gmres_solve(op, eta, psi0, cfg: GmresConfig) -> GmresResult:
     nop = None
     if reduce is None and not cfg.reorthogonalize and NATIVE_ARNOLDI and hasattr(dop, "native_operator"):
         nop = dop.native_operator(z[0])
+    if cgs and nop is None:
+        raise ValueError("orthogonalization='cgs' runs in the library-issued Arnoldi step only: a single-rank "
+                         "stencil operator without reorthogonalize")
     rel_host = torch.empty(b, dtype=torch.float64, pin_memory=True) if nop is not None else None
     cycle = None
     if nop is not None and NATIVE_CYCLE:  # device-side stop test: one host round trip per cycle
@@ -399,7 +419,8 @@ def gamma_residual_audit(op, eta, psi0, cfg: GmresConfig) -> float:
     d_eta = upload(eta) if host else eta
     n, s, b = d_eta.n_sites, d_eta.s, d_eta.b
     m = cfg.restart_len
-    st = _State(b, m, cfg.breakdown_rel, dev)
+    cgs = cfg.orthogonalization == "cgs"
+    st = _State(b, m, cfg.breakdown_rel, dev, cgs=cgs)
     L = _lib.load()
     stream = stream_ptr()
     psi = d_eta.zeros_like() if psi0 is None else (upload(psi0) if host else psi0.copy())

@@ -327,3 +327,33 @@ def test_device_cycle_bitwise_equals_per_step(case, monkeypatch):
         assert a.iterations % 16 != 0  # converged inside a cycle
     assert np.array_equal(np.array(a.result.history), np.array(b.result.history))
     assert np.array_equal(a.psi.ksi(), b.psi.ksi())
+
+
+@pytest.mark.parametrize("oe", [False, True])
+def test_cgs_extension_matches_reference_goldens(oe):
+    """The classical Gram-Schmidt extension against the reference's MGS goldens
+    (8x4^3 near-unit, b=12, GMRES(30), tol 1e-10): iterations +-1, residual below
+    tol, solution equal to the oracle's to 1e-8."""
+    g = load_gmres()[f"nearunit_8444_{'oe' if oe else 'full'}"]
+    dims = tuple(g["dims"])
+    geom = P.LatticeGeometry(dims)
+    links = O.flip_time_boundary(O.near_unit_gauge(dims, g["eps"], g["link_seed"]), dims)
+    eta = host_field(O.gen_spinor(geom.n_sites, g["b"], g["eta_seed"]), 2, geom)
+    cfg = P.GmresConfig(restart_len=g["restart_len"], restarts=g["restarts"], tol=g["tol"], orthogonalization="cgs")
+    rep = P.solve_dirac(P.DiracParams(m0=g["m0"]), P.GaugeField(geom, links), None, eta, cfg, odd_even=oe)
+    assert abs(rep.iterations - g["iterations"]) <= 1
+    assert np.all(rep.full_relnorms <= g["tol"])
+    ref_h = np.array(g["history"])
+    k = min(len(ref_h), len(rep.result.history))
+    assert np.all(np.abs(np.array(rep.result.history[:k]) - ref_h[:k]) <= 1e-4 * ref_h[:k])
+    psi, _, _ = O.solve_dirac(dims, g["m0"], links, None, eta.ksi(),
+                              O.GmresConfig(restart_len=g["restart_len"], restarts=g["restarts"], tol=g["tol"]),
+                              odd_even=oe)
+    assert np.abs(rep.psi.ksi() - psi).max() / np.abs(psi).max() < 1e-8
+
+
+def test_cgs_extension_rejects_unsupported_paths():
+    m = P.matrix_op(np.eye(12 * 16, dtype=np.complex128))
+    eta = host_field(np.ones((16, 12, 2), dtype=np.complex128), 2)
+    with pytest.raises(ValueError, match="cgs"):
+        P.gmres_solve(m, eta, None, P.GmresConfig(orthogonalization="cgs"))

@@ -40,3 +40,27 @@ def test_cfg3_solve_matches_reference(key):
     k = min(len(ref_h), len(rep.result.history))
     got_h = np.array(rep.result.history[:k])
     assert np.all(np.abs(got_h - ref_h[:k]) <= 1e-6 * ref_h[:k])
+
+
+@pytest.mark.parametrize("key", ["proxy_24x12c_full", "proxy_24x12c_oe", "mid_32x16c_full"])
+def test_cfg3_cgs_extension_matches_reference_iterations(key):
+    """GmresConfig.orthogonalization='cgs' (classical Gram-Schmidt, a B200
+    extension): same iteration count as the reference's MGS solve (+-1), full-
+    system residual below tol, and the residual history within 1e-4 relative of
+    the reference's (CGS rounds differently; its orthogonality loss is
+    O(eps kappa^2))."""
+    from paper_2601_05816_b200.device import upload
+    g = _gold(key)
+    geom = P.LatticeGeometry(tuple(g["dims"]))
+    gauge = P.flip_time_boundary(P.near_unit_gauge(geom, g["eps"], g["link_seed"]))
+    eta = P.gen_spinor(geom.n_sites, g["b"], P.Layout.COMPONENT_MAJOR, seed=g["eta_seed"], geom=geom)
+    cfg = P.GmresConfig(restart_len=g["restart_len"], restarts=g["restarts"], tol=g["tol"], orthogonalization="cgs")
+    rep = P.solve_dirac(P.DiracParams(m0=g["m0"]), gauge, None, upload(eta), cfg, odd_even=g["odd_even"])
+    assert abs(rep.iterations - g["iterations"]) <= 1, (rep.iterations, g["iterations"])
+    assert np.all(np.asarray(rep.full_relnorms) <= g["tol"])
+    ref_h = np.array(g["history"])
+    k = min(len(ref_h), len(rep.result.history))
+    got_h = np.array(rep.result.history[:k])
+    dev = float(np.max(np.abs(got_h - ref_h[:k]) / ref_h[:k]))
+    print(f"{key}: cgs {rep.iterations} it vs reference {g['iterations']}, history max rel dev {dev:.2e}")
+    assert dev <= 1e-4

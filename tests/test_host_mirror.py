@@ -103,6 +103,9 @@ def test_gmres_config_and_ledger():
         P.GmresConfig(restart_len=0)
     with pytest.raises(ValueError):
         P.GmresConfig(tol=0.0)
+    with pytest.raises(ValueError, match="orthogonalization"):
+        P.GmresConfig(orthogonalization="householder")
+    assert P.GmresConfig().orthogonalization == "mgs"  # the reference's MGS by default
     assert account_traffic(1) == {"flops_per_site": 2574, "bytes_per_site": 4512}
     assert account_traffic(16) == {"flops_per_site": 41184, "bytes_per_site": 44832}
     assert FlopCounter(cmul=2, cadd=3, rmul=4).total_flops == 26
