@@ -179,7 +179,7 @@ def cmd_solve(args) -> int:
     _header(cfg)
     geom, gauge, clover, eta = _problem(cfg)
     gcfg = GmresConfig(restart_len=cfg.restart_len, restarts=cfg.restarts, tol=cfg.tol,
-                       fixed_iterations=cfg.fixed_iterations)
+                       fixed_iterations=cfg.fixed_iterations, orthogonalization=cfg.orthogonalization)
     comm = None
     if any(g > 1 for g in cfg.grid):
         grid = RankGrid(tuple(cfg.grid))

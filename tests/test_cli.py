@@ -43,6 +43,13 @@ def test_config_canonical_form_and_extensions():
     C.set_key(cfg, "device.dtype", "c64")
     assert C.canonical(cfg).endswith("device.dtype = c64\n")
     assert C.parse_config(C.canonical(cfg)) == cfg  # round trip
+    assert "solver.orthogonalization" not in C.canonical(cfg)
+    C.set_key(cfg, "solver.orthogonalization", "cgs")
+    assert C.canonical(cfg).endswith("solver.orthogonalization = cgs\n")
+    assert C.parse_config(C.canonical(cfg)) == cfg
+    C.set_key(cfg, "solver.orthogonalization", "qr")
+    with pytest.raises(C.ConfigError, match="orthogonalization"):
+        C.validate(cfg)
 
 
 def test_usage_errors_exit_1(capsys):
