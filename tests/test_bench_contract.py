@@ -8,6 +8,8 @@ import subprocess
 import sys
 from pathlib import Path
 
+import pytest
+
 ROOT = Path(__file__).resolve().parents[1]
 KEYS = {"impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
         "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"}
@@ -44,3 +46,20 @@ def test_reference_arm_under_torchrun_rank0_only():
     assert r.returncode == 0, r.stderr[-2000:]
     (line,) = _lines(r.stdout)
     assert line["n_gpus"] == 2 and line["config"]["lattice"] == [64, 16, 16, 16]
+
+
+@pytest.mark.gpu
+def test_own_arm_line_on_gpu():
+    """bench.py's own arm (GMRES records skipped for time): the driver's keys, the
+    roofline and e2e objects, the clocks line and a launch count."""
+    r = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--no-gmres"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    (line,) = _lines(r.stdout)
+    assert (KEYS - {"impl"}) | {"roofline", "gpu_launches", "clocks"} <= set(line)
+    assert line["config"]["lattice"] == [32, 16, 16, 16] and line["dtype"] == "c128"
+    roof = line["roofline"]
+    assert roof["bound"] == "hbm" and 0 < roof["frac"] < 1 and abs(roof["achieved"] / roof["peak"] - roof["frac"]) < 1e-9
+    assert line["e2e"]["h2d_bytes_per_step"] == line["e2e"]["d2h_bytes_per_step"] == 32 * 16 ** 3 * 12 * 16 * 16
+    assert 0 < line["e2e"]["value"] < line["value"] and line["gpu_launches"] >= 3
+    assert line["cpu_baseline"]["cores"] >= 1 and line["cpu_baseline"]["value"] > 0
