@@ -27,7 +27,8 @@ _LAZY = {
     "batched_vs_independent_audit": "gmres", "gamma_residual_audit": "gmres",
     "block_axpy": "blas", "block_scale": "blas", "block_norms": "blas", "block_dot": "blas",
     "DeviceField": "device", "DeviceGauge": "device", "upload": "device", "download": "device",
-    "upload_gauge": "device",
+    "upload_gauge": "device", "upload_packed_blocks": "device", "freeze": "device",
+    "ThreadGroup": "tsplit", "HaloTimeoutError": "tsplit",
     "TSplitComm": "tsplit",
     "MultiRankExecutor": "multirank", "apply_dirac_multirank": "multirank", "EpochStats": "multirank",
     "RunConfig": "config", "ConfigError": "config", "parse_config": "config", "load_config": "config",

@@ -22,14 +22,25 @@ DOT_STRATEGIES = ("naive", "deferred")
 _scratch: dict = {}
 
 
-def reduce_scratch(b: int, device=None) -> torch.Tensor:
-    """Zero-initialised reduction scratch for rhs count b (one per device/b)."""
+def new_reduce_scratch(b: int, device=None) -> torch.Tensor:
+    """A private zero-initialised reduction scratch (partials + last-block ticket)."""
     dev = device or require_device()
-    key = (str(dev), b)
+    nbytes = int(_lib.load().b200wd_reduce_scratch_bytes(b))
+    return torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+
+
+def reduce_scratch(b: int, device=None) -> torch.Tensor:
+    """Reduction scratch for rhs count b, one per (device, stream, b).
+
+    The reduction kernels fold their block partials with a last-block atomic
+    ticket in this buffer, so two reductions may share it only when they are
+    ordered on one stream; keying by the current stream keeps concurrent
+    reductions on different streams apart."""
+    dev = device or require_device()
+    key = (str(dev), torch.cuda.current_stream(dev).cuda_stream, b)
     t = _scratch.get(key)
     if t is None:
-        nbytes = int(_lib.load().b200wd_reduce_scratch_bytes(b))
-        t = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        t = new_reduce_scratch(b, dev)
         _scratch[key] = t
     return t
 

@@ -727,31 +727,14 @@ static bool sweep_single_launch(const b200wd_gmres_state* st, int j, int64_t n_s
   const bool cgs = st->orth == B200WD_ORTH_CGS;
   const size_t smem = cgs ? red_smem(st->b) + (size_t)st->m * st->b * sizeof(double2) : red_smem(st->b);
   const void* kern = cgs ? (const void*)arnoldi_cgs_kernel : (const void*)arnoldi_sweep_kernel;
-  static int sm_count = 0, occ[kBlock + 1] = {0};
-  if (sm_count == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
-    int coop = 0;
-    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-    if (!coop) en = 0;
-  }
-  if (!en) return false;
-  int occupancy = 0;
-  if (cgs) {  // smem depends on m: no cache
-    if (smem > 48 * 1024 ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occupancy, arnoldi_cgs_kernel, blk.x * blk.y, smem) !=
-            cudaSuccess)
-      occupancy = -1;
-  } else {
-    if (occ[st->b] == 0) {
-      int c = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, arnoldi_sweep_kernel, blk.x * blk.y, smem) != cudaSuccess)
-        c = -1;
-      occ[st->b] = c > 0 ? c : -1;
-    }
-    occupancy = occ[st->b];
-  }
+  LaunchFacts f;
+  if (cgs && smem > 48 * 1024) return false;
+  if (!launch_facts(kern, blk.x * blk.y, smem, f)) return false;
+  int dev = 0, coop = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop) return false;
+  const int occupancy = f.occ, sm_count = f.sm_count;
   if (occupancy <= 0 || (int64_t)occupancy * sm_count < grid) return false;
   ZList zl{};
   for (int p = 0; p <= j + 1; ++p) zl.z[p] = static_cast<const double2*>(z[p]);

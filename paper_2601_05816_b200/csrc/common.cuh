@@ -10,6 +10,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "libb200wd targets sm_100a only"
 #endif
@@ -181,5 +185,47 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
+}
+}  // namespace b200wd
+
+// ---- per-device launch facts (host) -----------------------------------------
+// A process may drive several GPUs (and several host threads may launch), so
+// the dynamic shared-memory attribute, the occupancy of a (kernel, block,
+// smem) shape and the SM count are cached per device ordinal under a mutex.
+namespace b200wd {
+struct LaunchFacts {
+  int occ = 0;       // resident CTAs per SM (0: the shape does not fit)
+  int sm_count = 0;  // SMs of the current device
+};
+inline bool launch_facts(const void* fn, int threads, size_t smem, LaunchFacts& out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, size_t>, LaunchFacts> facts;
+  static std::map<std::pair<const void*, int>, size_t> attr;  // dynamic smem attribute set per (kernel, device)
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(fn, dev, threads, smem);
+  auto it = facts.find(key);
+  if (it != facts.end()) {
+    out = it->second;
+    return out.occ > 0;
+  }
+  size_t& a = attr[std::make_pair(fn, dev)];
+  if (smem > 48 * 1024 && a < smem) {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    a = smem;
+  }
+  LaunchFacts f;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f.occ, fn, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    f.occ = 0;
+  }
+  cudaDeviceGetAttribute(&f.sm_count, cudaDevAttrMultiProcessorCount, dev);
+  facts[key] = f;
+  out = f;
+  return f.occ > 0;
 }
 }  // namespace b200wd

@@ -661,8 +661,6 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
   }
 }
 
-static int g_sm_count = 0;
-
 // Ring configuration: site blocks per item (compile time) and ring depth
 // (runtime).  Default: whole z lines per item when that gives <= 256
 // consumer threads, a ring of ~100 KB per CTA (two CTAs per SM) or ~200 KB
@@ -740,30 +738,9 @@ static int64_t n_items_of(int64_t nblk) { return nblk / NB; }
 template <typename R, int V, int B, int NB, bool PAR, bool TILED, bool ZG, bool CLOV = false>
 static bool launch_ring_kernel(const HopParams& p, int64_t n_items, int S, size_t smem, cudaStream_t st) {
   using Sh = RingShape<R, V, B, NB, PAR>;
-  static size_t attr_smem = 0;
-  if (attr_smem < smem) {
-    if (cudaFuncSetAttribute(hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG, CLOV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-      return false;
-    attr_smem = smem;
-  }
-  static int occ[9] = {0};  // CTAs per SM by ring depth, queried once
-  if (occ[S] == 0) {
-    int c = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG, CLOV>, Sh::NT,
-                                                      smem) !=
-            cudaSuccess ||
-        c <= 0)
-      return false;
-    occ[S] = c;
-  }
-  static int sm_count = 0;
-  if (sm_count == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
-  }
-  int64_t grid = (int64_t)occ[S] * sm_count;
+  LaunchFacts f;
+  if (!launch_facts((const void*)hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG, CLOV>, Sh::NT, smem, f)) return false;
+  int64_t grid = (int64_t)f.occ * f.sm_count;
   if (grid > n_items) grid = n_items;
   hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG, CLOV><<<(unsigned)grid, Sh::NT, smem, st>>>(p, n_items, S);
   return true;

@@ -246,30 +246,10 @@ static bool launch_ring2_nb(const HopParams& p, int S, cudaStream_t st) {
     if (S > 8) S = 8;
     size_t smem = Sh::smem(S);
     while (smem > 227 * 1024 && S > 2) smem = Sh::smem(--S);
-    static size_t attr_smem = 0;
-    if (attr_smem < smem) {
-      if (cudaFuncSetAttribute(hop_ring2_kernel<R, V, B, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem) != cudaSuccess)
-        return false;
-      attr_smem = smem;
-    }
-    static int occ[9] = {0};
-    if (occ[S] == 0) {
-      int c = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, hop_ring2_kernel<R, V, B, NB>, Sh::NT, smem) !=
-              cudaSuccess ||
-          c <= 0)
-        return false;
-      occ[S] = c;
-    }
-    static int sm_count = 0;
-    if (sm_count == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
-    }
+    LaunchFacts f;
+    if (!launch_facts((const void*)hop_ring2_kernel<R, V, B, NB>, Sh::NT, smem, f)) return false;
     const int64_t n_items = nblk / (2 * NB);
-    int64_t grid = (int64_t)occ[S] * sm_count;
+    int64_t grid = (int64_t)f.occ * f.sm_count;
     if (grid > n_items) grid = n_items;
     hop_ring2_kernel<R, V, B, NB><<<(unsigned)grid, Sh::NT, smem, st>>>(p, n_items, S);
     return true;

@@ -600,30 +600,10 @@ template <typename R, int V, int B, int NB, int LY, bool ZG>
 static bool launch_ts_kernel(const HopParams& p, const TsGrid& g0, int S, int nch, int pf, cudaStream_t st) {
   using Sh = TsShape<R, V, B, NB, LY>;
   const size_t smem = Sh::smem(S);
-  static size_t attr_smem = 0;
-  if (attr_smem < smem) {
-    if (cudaFuncSetAttribute(hop_tstream_kernel<R, V, B, NB, LY, ZG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-      return false;
-    attr_smem = smem;
-  }
-  static int occ[9] = {0};
-  if (occ[S] == 0) {
-    int c = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, hop_tstream_kernel<R, V, B, NB, LY, ZG>, Sh::NT, smem) !=
-            cudaSuccess ||
-        c <= 0)
-      return false;
-    occ[S] = c;
-  }
-  static int sm_count = 0;
-  if (sm_count == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
-  }
+  LaunchFacts f;
+  if (!launch_facts((const void*)hop_tstream_kernel<R, V, B, NB, LY, ZG>, Sh::NT, smem, f)) return false;
   TsGrid g = g0;
-  const int64_t grid_max = (int64_t)occ[S] * sm_count;
+  const int64_t grid_max = (int64_t)f.occ * f.sm_count;
   g.nch = nch > 0 ? (nch > g.nT ? g.nT : nch) : ts_choose_nch(g.ncol, g.nT, grid_max, LY > 1 ? 4 : 5);
   g.n_units = g.ncol * g.nch;
   g.pf = pf < 0 ? 0 : pf;

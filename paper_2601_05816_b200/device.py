@@ -257,21 +257,22 @@ def upload_packed_blocks(packed: np.ndarray, dtype: str = "c128", stream=None) -
 
 
 class _GaugeCache:
-    """Upload each host GaugeField once per dtype.
+    """Device copies of host gauge / clover arrays, with exact invalidation.
 
-    The key is the identity of the numpy array; a cheap strided fingerprint
-    detects in-place modification (then the links are uploaded again).
+    The reference recomputes from the host arrays on every call, so an
+    in-place edit of ``gauge.data`` must be seen by the next apply.  A host
+    array is therefore cached only while it is read-only
+    (``arr.flags.writeable == False``, e.g. after :func:`freeze`): such an array
+    cannot change in place, and its identity (weakref) keys the entry.  A
+    writeable array is uploaded again on every call.  Callers that apply the
+    same links many times either freeze them or pass an explicit
+    :class:`DeviceGauge` / :class:`DeviceClover` handle (``upload_gauge``,
+    ``upload_packed_blocks``), which is never re-uploaded.
     """
 
     def __init__(self):
         self._entries: dict = {}
-
-    @staticmethod
-    def _fingerprint(arr: np.ndarray) -> tuple:
-        flat = arr.reshape(-1)
-        step = max(1, flat.size // 2048)
-        sample = flat[::step]
-        return (arr.ctypes.data, arr.shape, complex(sample.sum()), complex((sample * np.arange(sample.size)).sum()))
+        self.uploads = 0  # host -> device link/clover uploads issued (accounting, tests)
 
     def get(self, gauge, dtype: str) -> DeviceGauge:
         if isinstance(gauge, DeviceGauge):
@@ -284,26 +285,32 @@ class _GaugeCache:
         return self._get(clover.data, dtype, "clover", lambda: upload_packed_blocks(clover.data, dtype))
 
     def _get(self, arr, dtype, kind, make):
+        if not isinstance(arr, np.ndarray) or arr.flags.writeable:
+            self.uploads += 1
+            return make()
         key = (id(arr), dtype, kind)
-        fp = self._fingerprint(arr)
         hit = self._entries.get(key)
         if hit is not None:
-            ref, hfp, dg = hit
-            if ref() is arr and hfp == fp:
+            ref, dg = hit
+            if ref() is arr:
                 return dg
+        self.uploads += 1
         dg = make()
-        try:
-            ref = weakref.ref(arr)
-        except TypeError:
-            ref = (lambda a=arr: a)
-        self._entries[key] = (ref, fp, dg)
+        self._entries[key] = (weakref.ref(arr), dg)
         # drop entries whose arrays died
-        for k in [k for k, (r, _, _) in self._entries.items() if r() is None]:
+        for k in [k for k, (r, _) in self._entries.items() if r() is None]:
             del self._entries[k]
         return dg
 
     def clear(self) -> None:
         self._entries.clear()
+
+
+def freeze(field):
+    """Mark a host GaugeField / CloverField read-only so its device copy is
+    cached across calls (see :class:`_GaugeCache`); returns the field."""
+    field.data.flags.writeable = False
+    return field
 
 
 gauge_cache = _GaugeCache()

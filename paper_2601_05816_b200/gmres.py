@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .blas import block_dot_device, block_norm2_device, reduce_scratch
+from .blas import block_dot_device, block_norm2_device, new_reduce_scratch
 from .device import DeviceField, require_device, stream_ptr, upload
 from .dirac import DiracOperator, DiracParams
 from .fields import BlockSpinorField
@@ -106,7 +106,7 @@ class _State:
         self.brk = torch.zeros(b, dtype=torch.int32, device=dev)
         self.dot = torch.zeros(b, **c128)
         self.y = torch.zeros((b, m), **c128)
-        self.scratch = reduce_scratch(b, dev)
+        self.scratch = new_reduce_scratch(b, dev)  # owned by this solve: no cross-stream sharing
         st = _lib.GmresState()
         st.b, st.m, st.breakdown_rel = b, m, brk_rel
         for name, t in (("h_raw", self.h_raw), ("h", self.h), ("gamma", self.gamma), ("cs", self.cs),

@@ -21,6 +21,7 @@ Grids that split X, Y or Z raise ``NotImplementedError``.
 from __future__ import annotations
 
 import time
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -62,12 +63,16 @@ class MultiRankExecutor:
         self.epoch = 0
         self.last_stats: list[EpochStats] = []
         self._plan_key = None
+        self._plan_refs = (lambda: None,)
         self._plan = None
 
     def _plan_for(self, gauge, clover, dtype):
         from .tsplit import CudaHaloKernels
+        # reuse the uploaded slabs only for read-only host arrays (device._GaugeCache
+        # semantics: a writeable array may have changed in place since the last call)
+        frozen = not gauge.data.flags.writeable and (clover is None or not clover.data.flags.writeable)
         key = (gauge.geom.dims, id(gauge.data), None if clover is None else id(clover.data), dtype)
-        if self._plan_key == key:
+        if frozen and self._plan_key == key and self._plan_refs[0]() is gauge.data:
             return self._plan
         geom, ranks = gauge.geom, self.grid.grid[0]
         slabs = []
@@ -80,6 +85,7 @@ class MultiRankExecutor:
                 dc = upload_packed_blocks(clover.data[lo:hi], dtype)
             slabs.append((lg, t0, lo, hi, _lib.Lattice.make(lg.dims, t0), dg, dc))
         self._plan, self._plan_key = (slabs, CudaHaloKernels()), key
+        self._plan_refs = (weakref.ref(gauge.data),)
         return self._plan
 
     def apply_device(self, params, gauge, clover, psi: DeviceField, out: DeviceField | None = None,

@@ -23,13 +23,30 @@ so the full apply and the distributed Schur operator take it too.
 
 GMRES reductions are one ``all_reduce`` of the b partial sums per reducing pass.
 With one rank the split degenerates to the single-GPU periodic apply.
+
+Transports.  The face exchange and the reductions go through a transport:
+``DistTransport`` (``torch.distributed``: NCCL between GPUs, gloo on CPU) or
+``ThreadTransport``, the reference's in-process "threads" mode (halo.py:296-316,
+one Python thread per rank, ``CommunicatorSet`` / ``_Mailbox``): ranks are
+threads of one process sharing one device, every exchange is a host barrier
+plus device copies, so no kernel ever waits on another rank's kernel.  It runs
+the whole distributed solve (split hops, distributed Schur operator, the
+all-reduce flow of ``gmres_solve``) on a single GPU for testing.
+
+Failure detection and accounting (halo.py:43-53, 91-114): a receive that does
+not complete within ``timeout_s`` raises :class:`HaloTimeoutError` naming the
+rank, direction and face; ``stats`` keeps the reference's ``EpochStats``
+analogue per rank -- applies, bytes sent, host time spent waiting for halos,
+and the device time of the interior and boundary hops (CUDA events).
 The antiperiodic time boundary rides in the links of the rank that owns global
 slice T-1 (``fields.flip_time_boundary(..., t_global, t_origin)``).
 """
 
 from __future__ import annotations
 
+import threading
 import time
+from datetime import timedelta
 
 import numpy as np
 import torch
@@ -68,6 +85,108 @@ class CudaHaloKernels:
         return torch.empty((6, nf, b), dtype=t, device=device)
 
 
+class HaloTimeoutError(RuntimeError):
+    """A halo receive did not complete in time (halo.py:43-53)."""
+
+    def __init__(self, rank: int, mu: int, direction: str, timeout_s: float):
+        self.rank, self.mu, self.direction, self.timeout_s = rank, mu, direction, timeout_s
+        super().__init__(f"rank {rank}: halo receive mu={mu} from the {direction} neighbour timed out "
+                         f"after {timeout_s:.1f} s")
+
+
+class DistTransport:
+    """Face exchange and reductions over ``torch.distributed`` (NCCL / gloo)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+
+    def allreduce(self, t: torch.Tensor) -> None:
+        dist.all_reduce(_real_view(t), op=dist.ReduceOp.SUM, group=self.group)
+
+    def exchange(self, lam, chi, lam_in, chi_in, up: int, down: int):
+        # complex faces travel as their real views (NCCL has no complex dtype)
+        ops = [
+            dist.P2POp(dist.isend, _real_view(lam), down, self.group, tag=1),
+            dist.P2POp(dist.irecv, _real_view(lam_in), up, self.group, tag=1),
+            dist.P2POp(dist.isend, _real_view(chi), up, self.group, tag=2),
+            dist.P2POp(dist.irecv, _real_view(chi_in), down, self.group, tag=2),
+        ]
+        reqs = dist.batch_isend_irecv(ops)
+        # (lam_in from up, chi_in from down) per request, for error naming
+        return [(r, ("up", "down")[i // 2] if len(reqs) == 4 else "up") for i, r in enumerate(reqs)]
+
+    def wait(self, handles, timeout_s: float, rank: int) -> None:
+        for r, direction in handles:
+            try:
+                ok = r.wait(timeout=timedelta(seconds=timeout_s)) if timeout_s else r.wait()
+            except RuntimeError as e:  # gloo / NCCL report a timed-out or failed work item
+                if "imeout" in str(e) or "imed out" in str(e):
+                    raise HaloTimeoutError(rank, 0, direction, timeout_s) from e
+                raise
+            if ok is False:
+                raise HaloTimeoutError(rank, 0, direction, timeout_s)
+
+
+class ThreadGroup:
+    """Shared state of an in-process rank group (halo.py CommunicatorSet)."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots: list = [None] * world
+
+    def transport(self, rank: int) -> "ThreadTransport":
+        return ThreadTransport(self, rank)
+
+
+class ThreadTransport:
+    """One rank of a :class:`ThreadGroup` (a thread of this process).
+
+    Every operation synchronises the rank's current CUDA stream, meets the
+    other ranks at a host barrier and combines their tensors with device
+    copies in rank order, so every rank sees bit-identical sums."""
+
+    def __init__(self, group: ThreadGroup, rank: int):
+        self.g, self.rank, self.world = group, rank, group.world
+
+    def _sync(self, t):
+        if t.is_cuda:
+            torch.cuda.current_stream(t.device).synchronize()
+
+    def _meet(self, timeout_s: float, what: str):
+        try:
+            self.g.barrier.wait(timeout=timeout_s or None)
+        except threading.BrokenBarrierError:
+            raise HaloTimeoutError(self.rank, 0, what, timeout_s) from None
+
+    def allreduce(self, t: torch.Tensor, timeout_s: float = 120.0) -> None:
+        self._sync(t)
+        self.g.slots[self.rank] = t
+        self._meet(timeout_s, "allreduce")
+        acc = self.g.slots[0].clone()
+        for r in range(1, self.world):
+            acc += self.g.slots[r].to(acc.device)
+        self._sync(acc)
+        self._meet(timeout_s, "allreduce")
+        t.copy_(acc)
+        self._sync(t)
+
+    def exchange(self, lam, chi, lam_in, chi_in, up: int, down: int, timeout_s: float = 120.0):
+        self._sync(lam)
+        self.g.slots[self.rank] = (lam, chi)
+        self._meet(timeout_s, "exchange")
+        lam_in.copy_(self.g.slots[up][0])   # lambda face of slice 0 of rank+1
+        chi_in.copy_(self.g.slots[down][1])  # chi face of slice T-1 of rank-1
+        self._sync(lam_in)
+        self._meet(timeout_s, "exchange")
+        return []
+
+    def wait(self, handles, timeout_s: float, rank: int) -> None:
+        return None
+
+
 class TSplitComm:
     """T-only domain decomposition over the ranks of a process group.
 
@@ -76,10 +195,13 @@ class TSplitComm:
     :meth:`apply_dirac` / :meth:`operator` are the rank-local slabs.
     """
 
-    def __init__(self, global_geom: LatticeGeometry, group=None, kernels=None, device=None):
+    def __init__(self, global_geom: LatticeGeometry, group=None, kernels=None, device=None, transport=None,
+                 timeout_s: float = 300.0):
         self.group = group
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.transport = transport if transport is not None else DistTransport(group)
+        self.world = self.transport.world
+        self.rank = self.transport.rank
+        self.timeout_s = timeout_s
         self.global_geom = global_geom
         self.local_geom, self.t_origin = t_split(global_geom, self.world, self.rank)
         if self.world > 1 and self.local_geom.dims[0] < 2:
@@ -90,13 +212,16 @@ class TSplitComm:
         self.up = (self.rank + 1) % self.world
         self.down = (self.rank - 1) % self.world
         self._faces = {}
-        self.stats = {"applies": 0, "bytes_sent": 0}
+        # EpochStats analogue (halo.py:101-114): host seconds blocked on halos,
+        # device milliseconds of the interior and boundary hops
+        self.stats = {"applies": 0, "bytes_sent": 0, "wait_s": 0.0, "interior_ms": 0.0, "boundary_ms": 0.0}
+        self.timing = False  # set True to record the device hop times (adds event syncs)
 
     # -- plumbing -------------------------------------------------------------
     def allreduce(self, t: torch.Tensor) -> torch.Tensor:
         """Sum per-rank partial reductions (GMRES dots / norms) in place."""
         if self.world > 1:
-            dist.all_reduce(_real_view(t), op=dist.ReduceOp.SUM, group=self.group)
+            self.transport.allreduce(t)
         return t
 
     def _face_buffers(self, parity, b, dtype, device):
@@ -113,15 +238,8 @@ class TSplitComm:
             lam_in.copy_(lam)
             chi_in.copy_(chi)
             return []
-        # complex faces travel as their real views (NCCL has no complex dtype)
-        ops = [
-            dist.P2POp(dist.isend, _real_view(lam), self.down, self.group, tag=1),
-            dist.P2POp(dist.irecv, _real_view(lam_in), self.up, self.group, tag=1),
-            dist.P2POp(dist.isend, _real_view(chi), self.up, self.group, tag=2),
-            dist.P2POp(dist.irecv, _real_view(chi_in), self.down, self.group, tag=2),
-        ]
         self.stats["bytes_sent"] += 2 * lam.numel() * lam.element_size()
-        return dist.batch_isend_irecv(ops)
+        return self.transport.exchange(lam, chi, lam_in, chi_in, self.up, self.down)
 
     # -- the split hop ----------------------------------------------------------
     def hop(self, dst_parity, src, out, xself, alpha, beta, scale=None, gauge=None, clover=None, mode=0):
@@ -143,16 +261,42 @@ class TSplitComm:
         f = self._face_buffers(None if par < 0 else 1 - par, b, dtype, src.data.device)
         k.pack(self.lat, dtype, b, -1 if par < 0 else 1 - par, gauge, src, f["lam"], f["chi"])
         reqs = self.exchange(f["lam"], f["chi"], f["lam_in"], f["chi_in"])
+        ev = self._events() if self.timing else None
+        if ev:
+            ev[0].record()
         if T > 2:
             k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 1, T - 1, **extra)
-        for r in reqs:
-            r.wait()
-        k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 0, 1, f["lam_in"], f["chi_in"],
-              **extra)
-        k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, T - 1, T, f["lam_in"],
-              f["chi_in"], **extra)
+        if ev:
+            ev[1].record()
+        t_w = time.perf_counter()
+        self.transport.wait(reqs, self.timeout_s, self.rank)
+        self.stats["wait_s"] += time.perf_counter() - t_w
+        if ev:
+            ev[2].record()
+        # both boundary slices in one launch when they are the whole slab (T = 2),
+        # else one launch each
+        if T == 2:
+            k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 0, 2, f["lam_in"],
+                  f["chi_in"], **extra)
+        else:
+            k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 0, 1, f["lam_in"],
+                  f["chi_in"], **extra)
+            k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, T - 1, T, f["lam_in"],
+                  f["chi_in"], **extra)
+        if ev:
+            ev[3].record()
+            ev[3].synchronize()
+            self.stats["interior_ms"] += ev[0].elapsed_time(ev[1])
+            self.stats["boundary_ms"] += ev[2].elapsed_time(ev[3])
         self.stats["applies"] += 1
         return out
+
+    def _events(self):
+        if not torch.cuda.is_available():
+            return None
+        if not hasattr(self, "_ev"):
+            self._ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        return self._ev
 
     # -- reference comm protocol ----------------------------------------------------
     def bind(self, params, gauge, clover=None, dtype="c128"):
@@ -168,12 +312,7 @@ class TSplitComm:
         else:
             if clover.geom.dims != self.local_geom.dims:
                 raise ValueError(f"clover slab {clover.geom.dims} != local geometry {self.local_geom.dims}")
-            key = (id(clover.data), dtype)
-            if getattr(self, "_clover_key", None) != key:  # uploaded once per field and precision
-                from .device import upload_packed_blocks
-                self._clover_dev = upload_packed_blocks(np.asarray(clover.data), dtype)
-                self._clover_key = key
-            self.clover = self._clover_dev
+            self.clover = gauge_cache.get_clover(clover, dtype)  # exact invalidation (device._GaugeCache)
         return self
 
     def apply_device(self, v: DeviceField, out: DeviceField | None = None, scale=None) -> DeviceField:
