@@ -15,6 +15,7 @@ inverse.
 
 from __future__ import annotations
 
+import warnings
 import weakref
 from dataclasses import dataclass
 
@@ -176,7 +177,7 @@ def upload(field, dtype: str = "c128", stream=None, parity=None) -> DeviceField:
         return DeviceField(field.data.to(torch_dtype(dtype)), field.n, field.geom, field.parity, field.layout)
     dev = require_device()
     arr = _host_array(field)
-    raw = torch.from_numpy(arr).to(dev, non_blocking=True)
+    raw = _host_tensor(arr).to(dev, non_blocking=True)
     out = DeviceField.empty(field.n_sites, field.b, field.s, dtype, getattr(field, "geom", None), parity,
                             Layout(int(field.layout)))
     _lib.call("b200wd_spinor_import", ptr(raw), int(field.layout), field.n_sites, field.s, field.b,
@@ -218,13 +219,23 @@ class DeviceGauge:
         return "c128" if self.data.dtype == torch.complex128 else "c64"
 
 
+def _host_tensor(a: np.ndarray) -> torch.Tensor:
+    """CPU tensor view of a host array that is only read (frozen arrays are
+    read-only; torch warns about non-writable views but never writes here)."""
+    if a.flags.writeable:
+        return torch.from_numpy(a)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(a)
+
+
 def upload_gauge(gauge, dtype: str = "c128", stream=None) -> DeviceGauge:
     dev = require_device()
     data = np.ascontiguousarray(np.asarray(gauge.data, dtype=np.complex128))
     n = gauge.geom.n_sites
     if data.shape != (n, 4, 3, 3):
         raise ValueError(f"gauge data has shape {data.shape}, expected {(n, 4, 3, 3)}")
-    raw = torch.from_numpy(data.reshape(-1)).to(dev, non_blocking=True)
+    raw = _host_tensor(data.reshape(-1)).to(dev, non_blocking=True)
     out = torch.empty((4, n // SITE_BLOCK, 9, SITE_BLOCK), dtype=torch_dtype(dtype), device=dev)
     _lib.call("b200wd_gauge_import", ptr(raw), n, ptr(out), dtype_code(dtype), stream_ptr(stream))
     return DeviceGauge(out, gauge.geom)
@@ -250,7 +261,7 @@ def upload_packed_blocks(packed: np.ndarray, dtype: str = "c128", stream=None) -
     n = arr.shape[0]
     if arr.shape != (n, 2, 21) or n % SITE_BLOCK:
         raise ValueError(f"packed blocks have shape {arr.shape}; need (n, 2, 21) with n % 8 == 0")
-    raw = torch.from_numpy(arr.reshape(-1)).to(dev, non_blocking=True)
+    raw = _host_tensor(arr.reshape(-1)).to(dev, non_blocking=True)
     out = torch.empty((n // SITE_BLOCK, 42, SITE_BLOCK), dtype=torch_dtype(dtype), device=dev)
     _lib.call("b200wd_clover_import", ptr(raw), n, ptr(out), dtype_code(dtype), stream_ptr(stream))
     return DeviceClover(out, n)
