@@ -405,7 +405,9 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
       int cb_slot = 0, cb_first = 1;
       uint32_t cb_phase = 0;
       const uint32_t lz = (uint32_t)(p.Z / (8 * F * NB));
+      bool sync = TILED && p.wave_cnt != nullptr;
       for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        if (TILED && sync) sync = wave_wait(p, it, n_items);
         const int64_t gb0 = (p.d_begin >> 3) + (TILED ? item_nat(it, p, lz) : it) * NB;
         const BlkCoord c0 = block_coord(gb0 * 8 * F, p);
 #if B200WD_L2_PREFETCH
@@ -455,6 +457,7 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
         B200WD_PRODUCE(4)
         B200WD_PRODUCE(5)
 #undef B200WD_PRODUCE
+        if (TILED && p.wave_cnt != nullptr) wave_arrive(p, it);
       }
     }
     return;
@@ -687,7 +690,11 @@ static int ring_knob(const char* name, int dflt) {
 
 // A T slice of the source field larger than this is not reused from L2 by
 // the t+1 hop of the next slice (tools/bench_strong.py on 48^3 x 96).
-constexpr int64_t kSliceNoReuse = 48ll << 20;
+// (B200WD_SLICE_KB overrides: tests force the large-lattice paths on small lattices)
+static int64_t slice_noreuse() {
+  static const int64_t kb = ring_knob("B200WD_SLICE_KB", 48 * 1024);
+  return kb << 10;
+}
 
 // L2 budget for one T slice of a traversal patch (B200WD_TILE_KB, default
 // 24 MB; 0 = natural order everywhere).  The patch's t-1, t and t+1 slices
@@ -735,6 +742,80 @@ static void choose_tiles(HopParams& p, int F, int NB, size_t bytes_per_field_sit
 template <int NB>
 static int64_t n_items_of(int64_t nblk) { return nblk / NB; }
 
+// Per-device wave counters of the synchronised traversal (grown on demand,
+// zeroed on the launch stream before each launch that uses them).
+static int* wave_counters(int64_t n, cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<int, std::pair<int*, int64_t>> bufs;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& b = bufs[dev];
+  if (b.second < n) {
+    if (b.first) cudaFree(b.first);  // synchronous: only while growing
+    b.first = nullptr;
+    b.second = 0;
+    int64_t cap = 1 << 16;
+    while (cap < n) cap <<= 1;
+    if (cudaMalloc(&b.first, cap * sizeof(int)) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    b.second = cap;
+  }
+  if (cudaMemsetAsync(b.first, 0, n * sizeof(int), st) != cudaSuccess) return nullptr;
+  return b.first;
+}
+
+// Wave synchronisation of a patched (TILED) traversal: one wave per patch
+// slice (B200WD_WAVE=0 turns it off, B200WD_WAVE_SLACK sets the slack).
+static void setup_waves(HopParams& p, int64_t n_items, int lz, cudaStream_t st) {
+  static const int en = ring_knob("B200WD_WAVE", 1);
+  static const int slack = ring_knob("B200WD_WAVE_SLACK", 2);
+  p.wave_cnt = nullptr;
+  if (!en || p.tile_x == 0) return;
+  p.wave_items = (int64_t)p.tile_x * p.tile_y * lz;
+  p.wave_slack = slack < 1 ? 1 : slack;
+  const int64_t n_waves = (n_items + p.wave_items - 1) / p.wave_items;
+  p.wave_cnt = wave_counters(n_waves, st);
+}
+
+// Full-lattice patched order for lattices whose T slice exceeds the L2 reuse
+// limit: the largest patch (tile_x | X, tile_y | Y) whose three slices fit the
+// budget (B200WD_WAVE_KB per slice), most nearly square in lines.  Off by
+// default: on 48^3 x 96 (c128 nrhs 12) the synchronised patched order cuts the
+// DRAM reads from 81.5 to 43.8 GB per apply (ncu, profiles/r2_wave_ncu.txt) but
+// runs 23.2 ms against 22.0 ms for the natural order -- the patched item order
+// costs 17% on its own even on an L2-resident lattice and the per-wave waits
+// add more (tools/wave_cost.sh), while the natural order is DRAM-bound at 89%
+// of the copy peak with 1.94x the compulsory traffic.
+static void choose_full_tiles(HopParams& p, int NB, size_t bytes_per_site) {
+  static const int64_t kb = ring_knob("B200WD_WAVE_KB", 0);
+  p.tile_x = p.tile_y = p.tile_nt = 0;
+  if (kb <= 0 || p.Z % (8 * NB)) return;
+  if (p.d_begin % p.per_t || p.d_end % p.per_t) return;
+  const int64_t line_bytes = (int64_t)p.Z * (int64_t)bytes_per_site;
+  const int64_t budget = kb << 10;
+  int best_x = 0, best_y = 0;
+  double best = 1e30;
+  for (int tx = 1; tx <= p.X; ++tx) {
+    if (p.X % tx) continue;
+    for (int ty = 1; ty <= p.Y; ++ty) {
+      if (p.Y % ty || (int64_t)tx * ty * line_bytes > budget) continue;
+      const double perim = 1.0 / tx + 1.0 / ty;
+      if (perim < best - 1e-12) {
+        best = perim;
+        best_x = tx;
+        best_y = ty;
+      }
+    }
+  }
+  if (best_x == 0 || (best_x == p.X && best_y == p.Y)) return;
+  p.tile_x = best_x;
+  p.tile_y = best_y;
+  p.tile_nt = (int32_t)((p.d_end - p.d_begin) / p.per_t);
+}
+
 template <typename R, int V, int B, int NB, bool PAR, bool TILED, bool ZG, bool CLOV = false>
 static bool launch_ring_kernel(const HopParams& p, int64_t n_items, int S, size_t smem, cudaStream_t st) {
   using Sh = RingShape<R, V, B, NB, PAR>;
@@ -760,10 +841,12 @@ static bool launch_ring_nb(const HopParams& p_in, int64_t nblk, int S, cudaStrea
     // 48^3 x 96 every patch shape tried (1..8 x 48, 48 x 2..8, 6 x 12) was
     // 10-25% slower than the natural order
     const bool clov = p.clov_mode != 0;
-    if (PAR && !clov) choose_tiles(p, Sh::F, NB, site_bytes);
     const int64_t slice_bytes = (int64_t)(p.per_t / Sh::F) * (int64_t)site_bytes;
+    if (PAR && !clov) choose_tiles(p, Sh::F, NB, site_bytes);
+    // full lattice, T slice beyond L2 reuse: wave-synchronised patched order
+    if (!PAR && !clov && slice_bytes > slice_noreuse() && (8 * NB) <= p.Z) choose_full_tiles(p, NB, site_bytes);
     static const int hints = ring_knob("B200WD_L2HINT", 1);  // read once per process
-    p.hint_t1 = hints ? (p.tile_x ? 2 : (slice_bytes > kSliceNoReuse ? 1 : 0)) : 0;
+    p.hint_t1 = hints ? (p.tile_x ? 2 : (slice_bytes > slice_noreuse() ? 1 : 0)) : 0;
     p.hint_tm1 = hints;
     const bool whole_lines = (8 * Sh::F * NB) % p.Z == 0;
     if (S <= 0) S = (Sh::SLOT_BYTES >= 40 * 1024) ? (200 * 1024) / Sh::SLOT_BYTES : (100 * 1024) / Sh::SLOT_BYTES;
@@ -784,11 +867,10 @@ static bool launch_ring_nb(const HopParams& p_in, int64_t nblk, int S, cudaStrea
       }
       return false;
     }
-    if constexpr (PAR) {
-      if (p.tile_x) {
-        if (whole_lines) return launch_ring_kernel<R, V, B, NB, PAR, true, false>(p, ni, S, smem, st);
-        return launch_ring_kernel<R, V, B, NB, PAR, true, true>(p, ni, S, smem, st);
-      }
+    if (p.tile_x) {
+      setup_waves(p, ni, p.Z / (8 * Sh::F * NB), st);
+      if (whole_lines) return launch_ring_kernel<R, V, B, NB, PAR, true, false>(p, ni, S, smem, st);
+      return launch_ring_kernel<R, V, B, NB, PAR, true, true>(p, ni, S, smem, st);
     }
     if (whole_lines) return launch_ring_kernel<R, V, B, NB, PAR, false, false>(p, ni, S, smem, st);
     return launch_ring_kernel<R, V, B, NB, PAR, false, true>(p, ni, S, smem, st);

@@ -53,7 +53,37 @@ struct HopParams {
   // device stop flag of a GMRES cycle enqueued without host round trips
   // (b200wd_gmres_cycle): when *stop != 0 at launch the kernel does nothing
   const int* stop;
+  // wave-synchronised traversal (patched order, lattices whose T slice exceeds
+  // L2): items [k*wave_items, (k+1)*wave_items) form wave k (one patch slice);
+  // a producer issues no item of wave k before every item of wave k-wave_slack
+  // was issued (per-wave counters in wave_cnt, zeroed before the launch), so
+  // the CTAs march the patch's slices together and a block loaded as a t+1
+  // neighbour is still in L2 when it is read as an own block and as a t-1
+  // neighbour.  Only a locality hint: the wait is bounded and never needed
+  // for correctness.  wave_cnt == nullptr: off.
+  int* wave_cnt;
+  int64_t wave_items;
+  int32_t wave_slack;
 };
+
+// bounded wait until wave w-slack is complete; false once a wait timed out
+// (then the caller stops synchronising: e.g. a CTA that is not co-resident)
+__device__ __forceinline__ bool wave_wait(const HopParams& p, int64_t it, int64_t n_items) {
+  const int64_t w = it / p.wave_items - p.wave_slack;
+  if (w < 0) return true;
+  const int64_t lo = w * p.wave_items;
+  const int need = (int)((lo + p.wave_items <= n_items ? p.wave_items : n_items - lo));
+  for (int i = 0; i < 4096; ++i) {  // <= ~0.5 ms
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p.wave_cnt + w) : "memory");
+    if (v >= need) return true;
+    __nanosleep(128);
+  }
+  return false;
+}
+__device__ __forceinline__ void wave_arrive(const HopParams& p, int64_t it) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(p.wave_cnt + it / p.wave_items) : "memory");
+}
 
 __device__ __forceinline__ bool hop_stopped(const HopParams& p) {
   return p.stop != nullptr && *static_cast<const volatile int*>(p.stop) != 0;
