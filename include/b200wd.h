@@ -69,6 +69,12 @@ const char* b200wd_last_error(void);
 /* Device properties the host needs for launch sizing (SM count, L2 bytes). */
 int b200wd_device_info(int device, int32_t* sm_count, int64_t* l2_bytes, int32_t* cc_major,
                        int32_t* cc_minor);
+/* SMs left free by the persistent (one-CTA-per-SM ring / stream) hop kernels
+ * launched from the calling thread: with sm_reserve = k their grid covers
+ * sm_count - k SMs, so kernels enqueued concurrently on other streams (NCCL's
+ * P2P halo exchange, halo.py:339-387's overlap) find resident room.  0 (the
+ * default) uses every SM.  Returns the previous value. */
+int b200wd_set_sm_reserve(int32_t sm_reserve);
 
 /* ---- layouts (fields.py:48-137, 156-161) -------------------------------- */
 /* Reference storage (complex128, Layout 1 rhs-major or 2 component-major,

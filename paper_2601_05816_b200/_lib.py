@@ -97,6 +97,7 @@ SIGNATURES = {
     "b200wd_abi_version": [],
     "b200wd_last_error": [],
     "b200wd_device_info": [C.c_int, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i32)],
+    "b200wd_set_sm_reserve": [_i32],
     "b200wd_spinor_import": [_vp, _i32, _i64, _i32, _i32, _vp, _i32, _vp],
     "b200wd_spinor_export": [_vp, _i32, _i64, _i32, _i32, _vp, _i32, _vp],
     "b200wd_gauge_import": [_vp, _i64, _vp, _i32, _vp],

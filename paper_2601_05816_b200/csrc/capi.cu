@@ -32,3 +32,10 @@ extern "C" int b200wd_device_info(int device, int32_t* sm_count, int64_t* l2_byt
   if (cc_minor) *cc_minor = p.minor;
   return B200WD_OK;
 }
+
+namespace b200wd {
+int persistent_sms(int sm_count) {
+  const int n = sm_count - g_sm_reserve;
+  return n < 1 ? 1 : n;
+}
+}  // namespace b200wd

@@ -13,6 +13,8 @@ void set_error(const char* fmt, ...);
 
 // stop flag of the GMRES cycle being enqueued on this thread (dirac.cu)
 extern thread_local const int* g_hop_stop;
+// SMs the persistent hop kernels launched from this thread leave free (dirac.cu)
+extern thread_local int g_sm_reserve;
 
 inline int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();

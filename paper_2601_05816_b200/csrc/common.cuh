@@ -228,4 +228,7 @@ inline bool launch_facts(const void* fn, int threads, size_t smem, LaunchFacts& 
   out = f;
   return f.occ > 0;
 }
+// SMs a persistent grid may cover: all of them less the calling thread's
+// reserve (b200wd_set_sm_reserve), at least one
+int persistent_sms(int sm_count);
 }  // namespace b200wd

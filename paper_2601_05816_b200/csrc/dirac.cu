@@ -21,6 +21,7 @@ namespace b200wd {
 // Stop flag of the GMRES cycle being enqueued on this thread (b200wd_gmres_cycle
 // sets it around its operator applications); nullptr everywhere else.
 thread_local const int* g_hop_stop = nullptr;
+thread_local int g_sm_reserve = 0;
 
 static int fill_params(HopParams& p, const b200wd_lattice* lat, int32_t dtype, int32_t b, int32_t parity) {
   B200WD_REQUIRE(lat != nullptr, "lattice descriptor is NULL");
@@ -51,6 +52,12 @@ static int fill_params(HopParams& p, const b200wd_lattice* lat, int32_t dtype, i
 }  // namespace b200wd
 
 using namespace b200wd;
+
+extern "C" int b200wd_set_sm_reserve(int32_t sm_reserve) {
+  const int prev = g_sm_reserve;
+  g_sm_reserve = sm_reserve < 0 ? 0 : sm_reserve;
+  return prev;
+}
 
 extern "C" int b200wd_hop(const b200wd_lattice* lat, int32_t dtype, int32_t b, int32_t dst_parity,
                           const void* links, const void* src, const void* xself, void* out, double alpha,

@@ -821,7 +821,7 @@ static bool launch_ring_kernel(const HopParams& p, int64_t n_items, int S, size_
   using Sh = RingShape<R, V, B, NB, PAR>;
   LaunchFacts f;
   if (!launch_facts((const void*)hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG, CLOV>, Sh::NT, smem, f)) return false;
-  int64_t grid = (int64_t)f.occ * f.sm_count;
+  int64_t grid = (int64_t)f.occ * persistent_sms(f.sm_count);
   if (grid > n_items) grid = n_items;
   hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG, CLOV><<<(unsigned)grid, Sh::NT, smem, st>>>(p, n_items, S);
   return true;

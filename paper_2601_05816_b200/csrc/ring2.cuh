@@ -249,7 +249,7 @@ static bool launch_ring2_nb(const HopParams& p, int S, cudaStream_t st) {
     LaunchFacts f;
     if (!launch_facts((const void*)hop_ring2_kernel<R, V, B, NB>, Sh::NT, smem, f)) return false;
     const int64_t n_items = nblk / (2 * NB);
-    int64_t grid = (int64_t)f.occ * f.sm_count;
+    int64_t grid = (int64_t)f.occ * persistent_sms(f.sm_count);
     if (grid > n_items) grid = n_items;
     hop_ring2_kernel<R, V, B, NB><<<(unsigned)grid, Sh::NT, smem, st>>>(p, n_items, S);
     return true;

@@ -603,7 +603,7 @@ static bool launch_ts_kernel(const HopParams& p, const TsGrid& g0, int S, int nc
   LaunchFacts f;
   if (!launch_facts((const void*)hop_tstream_kernel<R, V, B, NB, LY, ZG>, Sh::NT, smem, f)) return false;
   TsGrid g = g0;
-  const int64_t grid_max = (int64_t)f.occ * f.sm_count;
+  const int64_t grid_max = (int64_t)f.occ * persistent_sms(f.sm_count);
   g.nch = nch > 0 ? (nch > g.nT ? g.nT : nch) : ts_choose_nch(g.ncol, g.nT, grid_max, LY > 1 ? 4 : 5);
   g.n_units = g.ncol * g.nch;
   g.pf = pf < 0 ? 0 : pf;

@@ -44,6 +44,7 @@ slice T-1 (``fields.flip_time_boundary(..., t_global, t_origin)``).
 
 from __future__ import annotations
 
+import os
 import threading
 import time
 from datetime import timedelta
@@ -83,6 +84,11 @@ class CudaHaloKernels:
     def face_buffer(self, nf, b, dtype, device):
         t = torch.complex128 if dtype == "c128" else torch.complex64
         return torch.empty((6, nf, b), dtype=t, device=device)
+
+    def reserve_sms(self, k: int) -> int:
+        """Leave k SMs free for the persistent hop kernels launched next from
+        this thread (b200wd_set_sm_reserve); returns the previous value."""
+        return int(_lib.load().b200wd_set_sm_reserve(int(k)))
 
 
 class HaloTimeoutError(RuntimeError):
@@ -202,6 +208,10 @@ class TSplitComm:
         self.world = self.transport.world
         self.rank = self.transport.rank
         self.timeout_s = timeout_s
+        # SMs the interior hop leaves free while the halos are in flight, so
+        # NCCL's P2P kernels are resident next to the persistent ring kernel
+        # (B200WD_HALO_SMS, default 8)
+        self.sm_reserve = int(os.environ.get("B200WD_HALO_SMS", "8"))
         self.global_geom = global_geom
         self.local_geom, self.t_origin = t_split(global_geom, self.world, self.rank)
         if self.world > 1 and self.local_geom.dims[0] < 2:
@@ -214,7 +224,8 @@ class TSplitComm:
         self._faces = {}
         # EpochStats analogue (halo.py:101-114): host seconds blocked on halos,
         # device milliseconds of the interior and boundary hops
-        self.stats = {"applies": 0, "bytes_sent": 0, "wait_s": 0.0, "interior_ms": 0.0, "boundary_ms": 0.0}
+        self.stats = {"applies": 0, "bytes_sent": 0, "wait_s": 0.0, "interior_ms": 0.0, "boundary_ms": 0.0,
+                      "launches": 0}
         self.timing = False  # set True to record the device hop times (adds event syncs)
 
     # -- plumbing -------------------------------------------------------------
@@ -257,6 +268,7 @@ class TSplitComm:
         extra = {} if clover is None else {"clover": clover, "mode": mode}
         if self.world == 1:
             k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 0, T, **extra)
+            self.stats["launches"] += 1
             return out
         f = self._face_buffers(None if par < 0 else 1 - par, b, dtype, src.data.device)
         k.pack(self.lat, dtype, b, -1 if par < 0 else 1 - par, gauge, src, f["lam"], f["chi"])
@@ -265,7 +277,12 @@ class TSplitComm:
         if ev:
             ev[0].record()
         if T > 2:
-            k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 1, T - 1, **extra)
+            prev = k.reserve_sms(self.sm_reserve) if hasattr(k, "reserve_sms") else None
+            try:
+                k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 1, T - 1, **extra)
+            finally:
+                if prev is not None:
+                    k.reserve_sms(prev)
         if ev:
             ev[1].record()
         t_w = time.perf_counter()
@@ -289,6 +306,8 @@ class TSplitComm:
             self.stats["interior_ms"] += ev[0].elapsed_time(ev[1])
             self.stats["boundary_ms"] += ev[2].elapsed_time(ev[3])
         self.stats["applies"] += 1
+        # pack + interior (T > 2) + boundary slices (one launch when T == 2)
+        self.stats["launches"] += 1 + (1 if T > 2 else 0) + (1 if T == 2 else 2)
         return out
 
     def _events(self):
@@ -325,15 +344,20 @@ class TSplitComm:
             return self.apply_device(v)
         return self.apply_device(upload(v, self.dtype)).to_host(v.layout)
 
-    def apply_dirac(self, params, gauge, clover, psi, flops=None, perf=None):
-        """dirac.py:313-314 seam: psi and gauge are this rank's T slab."""
+    def apply_dirac(self, params, gauge, clover, psi, flops=None, perf=None, out=None):
+        """dirac.py:313-314 seam: psi and gauge are this rank's T slab.
+        ``out`` (a host BlockSpinorField of psi's shape) receives a host result
+        in place, as ``dirac.apply_dirac(..., out=)`` does."""
         if psi.s != SPINOR_LEN or psi.n_sites != self.local_geom.n_sites:
             raise ValueError(f"field has {psi.n_sites} sites / s={psi.s}; local slab has "
                              f"{self.local_geom.n_sites} sites")
         t0 = time.perf_counter()
         dtype = psi.dtype if isinstance(psi, DeviceField) else "c128"
         self.bind(params, gauge, clover, dtype)
-        res = self(psi)
+        if out is not None and not isinstance(psi, DeviceField):
+            res = self.apply_device(upload(psi, self.dtype)).to_host(out.layout, out=out)
+        else:
+            res = self(psi)
         if flops is not None:
             flops.add_apply(psi.n_sites, psi.b)
         if perf is not None:

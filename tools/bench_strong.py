@@ -85,6 +85,135 @@ def single_gpu_apply(gdims=GDIMS, dtypes=("c128", "c64"), b=12, steps=30, warmup
             "records": out, "link_gen_s": round(gen_s, 2), "l2": "fields 24.5 GB (c128) >> L2"}
 
 
+def split_apply_records(comm, gdims, b, dtypes, steps, warmup, grp, dev, base_n1=False):
+    """D_W apply of the T-split global lattice `gdims` (each rank its slab of
+    `comm`), random device fields and links (kernel time does not depend on
+    the values).  Times are max over ranks (``grp.max``).  With ``base_n1``
+    rank 0 also times the whole lattice on its own GPU (the strong-scaling
+    base point from the same code, same run), while the other ranks wait."""
+    from paper_2601_05816_b200.device import DeviceGauge
+    lg, world = comm.local_geom, comm.world
+    n = lg.n_sites
+    peak = hbm_peak()
+    out = []
+    for dt in dtypes:
+        tdt = torch.complex128 if dt == "c128" else torch.complex64
+        g = torch.Generator(device=dev).manual_seed(7 + comm.rank)
+        links = torch.randn((4, n // 8, 9, 8), dtype=tdt, device=dev, generator=g)
+        comm.bind(P.DiracParams(m0=M0), DeviceGauge(links, lg), None, dt)
+        psi = DeviceField(torch.randn((n // 8, 12, 8, b), dtype=tdt, device=dev, generator=g), n, lg)
+        eta = psi.empty_like()
+        for _ in range(warmup):
+            comm.apply_device(psi, eta)
+        torch.cuda.synchronize()
+        grp.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            comm.apply_device(psi, eta)
+        e1.record()
+        torch.cuda.synchronize()
+        t = grp.max(e0.elapsed_time(e1) * 1e-3 / steps)
+        # per-rank halo accounting of one extra apply (EpochStats analogue, halo.py:101-114)
+        comm.timing = True
+        st0 = dict(comm.stats)
+        comm.apply_device(psi, eta)
+        comm.timing = False
+        ep = {k: comm.stats[k] - st0[k] for k in ("wait_s", "interior_ms", "boundary_ms")}
+        ep["rank"] = comm.rank
+        alg = compulsory_bytes_per_site(b, dt) * n
+        rec = {"dtype": dt, "nrhs": b, "n_gpus": world, "local": list(lg.dims), "ms": round(t * 1e3, 4),
+               "site_rhs_per_s": world * n * b / t, "hbm_gbs_per_gpu": round(alg / t / 1e9, 1),
+               "frac_per_gpu": round(alg / t / 1e9 / peak, 4), "epoch_stats": grp.gather(ep)}
+        del psi, eta, links
+        comm.gauge = None
+        torch.cuda.empty_cache()
+        if base_n1 and world > 1:
+            grp.barrier()
+            if comm.rank == 0:
+                gg = P.LatticeGeometry(tuple(gdims))
+                ng = gg.n_sites
+                gl = torch.randn((4, ng // 8, 9, 8), dtype=tdt, device=dev, generator=g)
+                x = DeviceField(torch.randn((ng // 8, 12, 8, b), dtype=tdt, device=dev, generator=g), ng, gg)
+                y = x.empty_like()
+                op = P.DiracOperator(P.DiracParams(m0=M0), DeviceGauge(gl, gg), None, dt)
+                for _ in range(warmup):
+                    op.apply_device(x, y)
+                torch.cuda.synchronize()
+                e0.record()
+                for _ in range(steps):
+                    op.apply_device(x, y)
+                e1.record()
+                torch.cuda.synchronize()
+                t1 = e0.elapsed_time(e1) * 1e-3 / steps
+                rec["base_n1_ms"] = round(t1 * 1e3, 4)
+                rec["strong_efficiency"] = round(t1 / (world * t), 4)
+                del gl, x, y, op
+                torch.cuda.empty_cache()
+            grp.barrier()
+        out.append(rec)
+    return out
+
+
+def split_gmres(comm, gdims, b, grp, dev, restart_len=8, tol=1e-8, eps=0.3):
+    """configs[4] odd-even batched GMRES(8) to tol 1e-8 on the T split:
+    near-unit links (this rank's slab, generated per T slice), Gaussian rhs,
+    TSplitComm.solve_dirac(odd_even=True) (reduce_rhs, distributed Schur
+    GMRES with all-reduced reductions, reconstruct, full-system residual)."""
+    lg, t0 = comm.local_geom, comm.t_origin
+    tg = time.perf_counter()
+    links = P.near_unit_links(gdims, eps, 0, t0, t0 + lg.dims[0],
+                              workers=max(1, (os.cpu_count() or 1) // max(1, comm.world)))
+    gauge = P.flip_time_boundary(P.GaugeField(lg, links), gdims[0], t0)
+    del links
+    gen_s = time.perf_counter() - tg
+    n = lg.n_sites
+    g = torch.Generator(device=dev).manual_seed(100 + comm.rank)
+    eta = DeviceField(torch.randn((n // 8, 12, 8, b), dtype=torch.complex128, device=dev, generator=g), n, lg)
+    cfg = P.GmresConfig(restart_len=restart_len, restarts=250, tol=tol)
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats(dev)
+    grp.barrier()
+    t1 = time.perf_counter()
+    rep = comm.solve_dirac(P.DiracParams(m0=M0), gauge, None, eta, cfg, odd_even=True)
+    torch.cuda.synchronize()
+    tts = grp.max(time.perf_counter() - t1)
+    return {"workload": "BASELINE configs[4] odd-even batched GMRES(8), tol 1e-8", "lattice": list(gdims),
+            "n_gpus": comm.world, "nrhs": b, "iterations": rep.iterations, "time_to_solution_s": tts,
+            "ms_per_iteration": tts / max(rep.iterations, 1) * 1e3,
+            "max_full_relnorm": float(grp.max(float(max(rep.full_relnorms)))),
+            "converged": bool(max(rep.full_relnorms) <= tol), "link_gen_s": round(gen_s, 2),
+            "peak_mem_gb_rank0": torch.cuda.max_memory_allocated(dev) / 1e9}
+
+
+class LocalGroup:
+    """One-rank stand-in of bench.py's rank group."""
+
+    rank, world = 0, 1
+
+    def barrier(self):
+        pass
+
+    def max(self, x):
+        return float(x)
+
+    def gather(self, obj):
+        return [obj]
+
+
+def single_gpu_gmres(gdims=GDIMS, b=12):
+    """configs[4]'s odd-even GMRES(8) to 1e-8 on one GPU (the N=1 point of
+    the strong-scaling solve): TSplitComm with one rank is the single-GPU path."""
+    from paper_2601_05816_b200.tsplit import TSplitComm
+    dev = torch.device("cuda", torch.cuda.current_device())
+    comm = TSplitComm(P.LatticeGeometry(tuple(gdims)))
+    rec = split_gmres(comm, tuple(gdims), b, LocalGroup(), dev)
+    from paper_2601_05816_b200.device import gauge_cache
+    gauge_cache.clear()
+    torch.cuda.empty_cache()
+    return rec
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--b", type=int, default=12)
