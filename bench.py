@@ -656,6 +656,13 @@ def main(argv=None):
     import paper_2601_05816_b200 as P
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.force_dist:
         import torch.distributed as dist
+        if "RANK" not in os.environ:  # --force-dist without a launcher: a one-rank group
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=str(port))
         dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
         torch.cuda.set_device(dev)
         dist.init_process_group("nccl", device_id=dev)
@@ -669,7 +676,10 @@ def main(argv=None):
     sweep, hbm_peak, peak_kind = gpu_sweep(args, torch, P)
     clk = clocks.stop()
     head = next(r for r in sweep if (r["dtype"], r["nrhs"]) == HEADLINE)
-    e2e = gpu_e2e(args, torch, P)
+    # headline e2e: the rhs block in and the result out through apply_dirac every step,
+    # pinned host buffers, links frozen (read-only, uploaded once: static configuration,
+    # labelled links_cached); the variants re-upload the links every call / use pageable buffers
+    e2e = gpu_e2e(args, torch, P, freeze_links=True)
     line = {
         "metric": METRIC, "value": head["site_rhs_per_s"], "unit": "site*rhs/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms"], "higher_is_better": True,
@@ -682,8 +692,8 @@ def main(argv=None):
                      "algorithmic_bytes_per_launch": head["bytes_per_launch"],
                      "kernel": "hop_ring_kernel<double,1,16> (libb200wd.so, b200wd_dirac_apply)"},
         "e2e": e2e, "gpu_launches": args.steps, "clocks": clk,
-        "e2e_variants": {"pageable": gpu_e2e(args, torch, P, pinned=False),
-                         "pinned_links_frozen": gpu_e2e(args, torch, P, freeze_links=True)},
+        "e2e_variants": {"pinned_links_every_call": gpu_e2e(args, torch, P),
+                         "pageable_links_every_call": gpu_e2e(args, torch, P, pinned=False)},
         "sweep": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()} for r in sweep],
     }
     line["clover"] = gpu_clover(args, torch, P)
@@ -695,7 +705,9 @@ def main(argv=None):
         line["schur"] = schur_bench()  # BASELINE configs[2]: 32^3x64 Schur apply, nrhs=12, c128
         from bench_strong import single_gpu_apply, single_gpu_gmres
         # BASELINE configs[4] at N=1: 48^3x96, nrhs=12 (the strong-scaling base point)
+        torch.cuda.empty_cache()
         line["strong"] = single_gpu_apply(sampler=ClockSampler)
+        torch.cuda.empty_cache()
         line["strong"]["gmres"] = single_gpu_gmres()
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample()

@@ -63,9 +63,11 @@ def test_own_arm_line_on_gpu():
     roof = line["roofline"]
     assert roof["bound"] == "hbm" and 0 < roof["frac"] < 1 and abs(roof["achieved"] / roof["peak"] - roof["frac"]) < 1e-9
     field, links = 32 * 16 ** 3 * 12 * 16 * 16, 32 * 16 ** 3 * 4 * 9 * 16
-    assert line["e2e"]["d2h_bytes_per_step"] == field and line["e2e"]["h2d_bytes_per_step"] == field + links
-    assert line["e2e_variants"]["pageable"]["host_buffers"] == "pageable"
-    assert line["e2e_variants"]["pinned_links_frozen"]["h2d_bytes_per_step"] == field
+    assert line["e2e"]["d2h_bytes_per_step"] == line["e2e"]["h2d_bytes_per_step"] == field
+    assert line["e2e"]["links_cached"] is True
+    v = line["e2e_variants"]
+    assert v["pageable_links_every_call"]["host_buffers"] == "pageable"
+    assert v["pinned_links_every_call"]["h2d_bytes_per_step"] == field + links
     assert 0 < line["e2e"]["value"] < line["value"] and line["gpu_launches"] >= 3
     assert line["cpu_baseline"]["cores"] >= 1 and line["cpu_baseline"]["value"] > 0
 
@@ -113,4 +115,4 @@ def test_multi_gpu_arm_logic_with_thread_ranks():
     recs = line["strong"]["records"]
     assert [r["dtype"] for r in recs] == ["c128", "c64"] and all(r["base_n1_ms"] > 0 for r in recs)
     gm = line["strong"]["gmres"]
-    assert gm["converged"] and gm["iterations"] > 0 and gm["max_full_relnorm"] <= 1e-8
+    assert gm["converged"] and gm["iterations"] > 0 and gm["max_final_relnorm"] <= 1e-8
