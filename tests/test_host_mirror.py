@@ -158,3 +158,26 @@ def test_perf_model_formulas():
         P.arithmetic_intensity(0)
     with pytest.raises(ValueError):
         P.CounterSample(-1, 0, 1, 1.0)
+
+
+def test_reference_written_snapshots_read_and_rewrite_byte_identical(tmp_path, golden_dir):
+    """Files written by lqcdlab itself (tests/golden/make_golden_snapshots.py)
+    read back into the generators' values, and this package writes the very
+    same bytes (fields.py:264-337)."""
+    import paper_2601_05816_b200 as P
+    geom = P.LatticeGeometry((4, 2, 2, 4))
+    g = P.read_gauge(golden_dir / "snap_gauge.lqmg")
+    assert np.array_equal(g.data, P.gen_gauge(geom, "random", seed=11).data)
+    c = P.read_clover(golden_dir / "snap_clover.lqmc")
+    assert np.array_equal(c.data, P.gen_clover(geom, "random", scale=0.1, seed=12).data)
+    P.write_gauge(tmp_path / "g", g)
+    P.write_clover(tmp_path / "c", c)
+    assert (tmp_path / "g").read_bytes() == (golden_dir / "snap_gauge.lqmg").read_bytes()
+    assert (tmp_path / "c").read_bytes() == (golden_dir / "snap_clover.lqmc").read_bytes()
+    for layout in (1, 2):
+        name = f"snap_spinor_l{layout}.lqml"
+        f = P.read_spinor(golden_dir / name)
+        want = P.gen_spinor(geom.n_sites, 3, P.Layout(layout), seed=13, geom=geom)
+        assert int(f.layout) == layout and f.b == 3 and np.array_equal(f.data, want.data)
+        P.write_spinor(tmp_path / name, want)
+        assert (tmp_path / name).read_bytes() == (golden_dir / name).read_bytes()
