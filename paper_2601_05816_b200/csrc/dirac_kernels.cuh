@@ -299,7 +299,7 @@ __device__ __forceinline__ int64_t item_nat(int64_t it, const HopParams& p, uint
 // tile H in 0..5: hop (mu = H/2, forward if H even); H == 6: own blocks (z tile).
 // PAR: checkerboard fields (a field block of 8 cb sites = 16 natural sites of
 // one z line, Z % 16 == 0); links are always natural-site blocks.
-template <typename R, int V, int B, int NB, bool PAR, int H>
+template <typename R, int V, int B, int NB, bool PAR, int H, bool HALO = false>
 __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, const BlkCoord& c0, cx<R>* slot,
                                            uint64_t* full, uint64_t pol_first, uint64_t pol_t1) {
   using C = cx<R>;
@@ -308,14 +308,33 @@ __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, cons
   const C* src = static_cast<const C*>(p.src);
   const C* U = static_cast<const C*>(p.U);
   const int64_t nblk = p.n >> 3;  // natural link blocks
-  mbar_expect_tx(full, (uint32_t)(Sh::SLOT * sizeof(C)));
   if constexpr (H == 6) {
+    mbar_expect_tx(full, (uint32_t)(Sh::SLOT * sizeof(C)));
     bulk_g2s(slot, src + gb0 * 96 * B, Sh::SPIN * sizeof(C), full);
     bulk_g2s(slot + Sh::SPIN, U + (3 * nblk + F * gb0) * 72, NB * Sh::LPB * sizeof(C), full);
   } else {
     constexpr int MU = H >> 1;
     constexpr bool FWD = !(H & 1);
+    if constexpr (HALO && H <= 1) {
+      // T-split boundary slice (halo.py:370-387): the t+1 neighbour of the last
+      // local slice is the lam face of rank+1, the t-1 neighbour of slice 0 the
+      // chi face of rank-1 -- 6 half-spinor components per face site, stored
+      // (6, nf, b); the item's NB*8 field sites are one run per component.
+      const void* face = H == 0 ? (c0.t + 1 == p.T ? p.lam_halo : nullptr) : (c0.t == 0 ? p.chi_halo : nullptr);
+      if (face != nullptr) {
+        const C* fp = static_cast<const C*>(face);
+        const int64_t i0 = gb0 * 8 - (int64_t)c0.t * (p.per_t / F);  // face index of the item's first field site
+        constexpr int RUN = NB * 8 * B;
+        mbar_expect_tx(full, (uint32_t)((6 * RUN + NB * Sh::LPB) * sizeof(C)));
+#pragma unroll
+        for (int k = 0; k < 6; ++k) bulk_g2s(slot + k * RUN, fp + (k * p.nf + i0) * B, RUN * sizeof(C), full);
+        // U_0 of the own blocks (the lam hop multiplies at the destination; unused by chi)
+        bulk_g2s(slot + Sh::SPIN, U + (0 * nblk + F * gb0) * 72, NB * Sh::LPB * sizeof(C), full);
+        return;
+      }
+    }
     // neighbour field blocks of the NB own blocks: contiguous unless a wrap falls inside the item
+    mbar_expect_tx(full, (uint32_t)(Sh::SLOT * sizeof(C)));
     const int64_t nb0 = block_neighbor<MU, FWD>(gb0 * 8 * F, c0, p) / (8 * F);
     bool contiguous = true;
     if constexpr (NB > 1) {
@@ -362,7 +381,7 @@ __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, cons
 constexpr int kClovBufs = 2;
 template <typename R, int NB> __host__ __device__ constexpr int clov_tile() { return NB * 336; }
 
-template <typename R, int V, int B, int NB, bool PAR, bool TILED, bool ZG, bool CLOV = false>
+template <typename R, int V, int B, int NB, bool PAR, bool TILED, bool ZG, bool CLOV = false, bool HALO = false>
 __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_kernel(const HopParams p,
                                                                                    int64_t n_items, int S) {
   using C = cx<R>;
@@ -430,7 +449,7 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
 #define B200WD_PRODUCE(H)                                                                   \
   {                                                                                         \
     if (pfirst == 0) mbar_wait(&empty[pslot], pphase ^ 1u);                                 \
-    ring_issue<R, V, B, NB, PAR, H>(p, gb0, c0, ring + pslot * Sh::SLOT, &full[pslot], pol_first, pol_t1); \
+    ring_issue<R, V, B, NB, PAR, H, HALO>(p, gb0, c0, ring + pslot * Sh::SLOT, &full[pslot], pol_first, pol_t1); \
     if (++pslot == S) {                                                                     \
       pslot = 0;                                                                            \
       pphase ^= 1u;                                                                         \
@@ -498,6 +517,8 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
     const int64_t nat0 = gb0 * 8 * F;        // natural base site of the item
     const int li = (int)(xn - nat0);         // natural index inside the item's link blocks
     const int lofs = (li >> 3) * 72 + (li & 7);
+    int item_t = -1;  // HALO: local slice of the item (items never straddle slices)
+    if constexpr (HALO) item_t = block_coord(nat0, p).t;
     C acc[V][12];
     {  // own blocks: xself, z hops
       const int slot = cslot;
@@ -581,7 +602,11 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
     const int slot = cslot;                                                                          \
     mbar_wait(&full[slot], cphase);                                                                  \
     const C* sb = ring + slot * Sh::SLOT;                                                            \
-    if (!B200WD_RING_NOMATH)                                                                         \
+    if (HALO && (H) == 0 && item_t == p.T - 1)                                                       \
+      hop_lam_halo<R, V, true, true>(acc, sb + (j * 8 + lo) * B + r0, NB * 8 * B, sb + Sh::SPIN + lofs, 8); \
+    else if (HALO && (H) == 1 && item_t == 0)                                                        \
+      hop_chi_halo<R, V, true>(acc, sb + (j * 8 + lo) * B + r0, NB * 8 * B);                         \
+    else if (!B200WD_RING_NOMATH)                                                                    \
       hop_full<((H) >> 1), !((H)&1), R, V, true, true>(acc, sb + j * 96 * B + lo * B + r0, KST,      \
                                                         sb + Sh::SPIN + lofs, 8);                    \
     __syncwarp();                                                                                    \
@@ -816,14 +841,15 @@ static void choose_full_tiles(HopParams& p, int NB, size_t bytes_per_site) {
   p.tile_nt = (int32_t)((p.d_end - p.d_begin) / p.per_t);
 }
 
-template <typename R, int V, int B, int NB, bool PAR, bool TILED, bool ZG, bool CLOV = false>
+template <typename R, int V, int B, int NB, bool PAR, bool TILED, bool ZG, bool CLOV = false, bool HALO = false>
 static bool launch_ring_kernel(const HopParams& p, int64_t n_items, int S, size_t smem, cudaStream_t st) {
   using Sh = RingShape<R, V, B, NB, PAR>;
   LaunchFacts f;
-  if (!launch_facts((const void*)hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG, CLOV>, Sh::NT, smem, f)) return false;
+  if (!launch_facts((const void*)hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG, CLOV, HALO>, Sh::NT, smem, f))
+    return false;
   int64_t grid = (int64_t)f.occ * persistent_sms(f.sm_count);
   if (grid > n_items) grid = n_items;
-  hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG, CLOV><<<(unsigned)grid, Sh::NT, smem, st>>>(p, n_items, S);
+  hop_ring_kernel<R, V, B, NB, PAR, TILED, ZG, CLOV, HALO><<<(unsigned)grid, Sh::NT, smem, st>>>(p, n_items, S);
   return true;
 }
 
@@ -841,10 +867,12 @@ static bool launch_ring_nb(const HopParams& p_in, int64_t nblk, int S, cudaStrea
     // 48^3 x 96 every patch shape tried (1..8 x 48, 48 x 2..8, 6 x 12) was
     // 10-25% slower than the natural order
     const bool clov = p.clov_mode != 0;
+    const bool halo = p.lam_halo != nullptr;  // T-split boundary slices: natural order, halo tiles
     const int64_t slice_bytes = (int64_t)(p.per_t / Sh::F) * (int64_t)site_bytes;
-    if (PAR && !clov) choose_tiles(p, Sh::F, NB, site_bytes);
+    if (PAR && !clov && !halo) choose_tiles(p, Sh::F, NB, site_bytes);
     // full lattice, T slice beyond L2 reuse: wave-synchronised patched order
-    if (!PAR && !clov && slice_bytes > slice_noreuse() && (8 * NB) <= p.Z) choose_full_tiles(p, NB, site_bytes);
+    if (!PAR && !clov && !halo && slice_bytes > slice_noreuse() && (8 * NB) <= p.Z)
+      choose_full_tiles(p, NB, site_bytes);
     static const int hints = ring_knob("B200WD_L2HINT", 1);  // read once per process
     p.hint_t1 = hints ? (p.tile_x ? 2 : (slice_bytes > slice_noreuse() ? 1 : 0)) : 0;
     p.hint_tm1 = hints;
@@ -862,10 +890,18 @@ static bool launch_ring_nb(const HopParams& p_in, int64_t nblk, int S, cudaStrea
         while (Sh::smem(S) + cextra > budget && S > 2) --S;
         smem = Sh::smem(S) + cextra;
         if (smem > 227 * 1024) return false;
+        if (halo) {
+          if (whole_lines) return launch_ring_kernel<R, V, B, NB, PAR, false, false, true, true>(p, ni, S, smem, st);
+          return launch_ring_kernel<R, V, B, NB, PAR, false, true, true, true>(p, ni, S, smem, st);
+        }
         if (whole_lines) return launch_ring_kernel<R, V, B, NB, PAR, false, false, true>(p, ni, S, smem, st);
         return launch_ring_kernel<R, V, B, NB, PAR, false, true, true>(p, ni, S, smem, st);
       }
       return false;
+    }
+    if (halo) {
+      if (whole_lines) return launch_ring_kernel<R, V, B, NB, PAR, false, false, false, true>(p, ni, S, smem, st);
+      return launch_ring_kernel<R, V, B, NB, PAR, false, true, false, true>(p, ni, S, smem, st);
     }
     if (p.tile_x) {
       setup_waves(p, ni, p.Z / (8 * Sh::F * NB), st);
@@ -948,7 +984,11 @@ static bool try_launch_ring_par(const HopParams& p, int64_t nblk, RingCfg c, cud
 template <typename R, int V, int B>
 static bool try_launch_ring(const HopParams& p, cudaStream_t st) {
   static const int ring_clover = ring_knob("B200WD_RING_CLOVER", 1);
-  if (p.lam_halo != nullptr || p.beta == 0.0) return false;
+  if (p.beta == 0.0) return false;
+  // boundary slices consuming halo faces: slice-aligned ranges only
+  if (p.lam_halo != nullptr && (p.d_begin % (p.dst_parity >= 0 ? p.per_t / 2 : p.per_t) ||
+                                p.d_end % (p.dst_parity >= 0 ? p.per_t / 2 : p.per_t)))
+    return false;
   if (p.clov_mode != 0 && (!ring_clover || sizeof(R) != 8 || (p.dst_parity >= 0 && p.clov_mode == 1)))
     return false;
   const bool par = p.dst_parity >= 0;

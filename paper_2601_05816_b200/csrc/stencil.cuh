@@ -243,7 +243,8 @@ __device__ __forceinline__ void hop_full(cx<R> (&acc)[V][12], const cx<R>* __res
 }
 
 // Forward T hop whose projected half spinor comes from the lam halo face.
-template <typename R, int V>
+// SS / SL: face / link in shared memory (the ring kernel's halo tiles).
+template <typename R, int V, bool SS = false, bool SL = false>
 __device__ __forceinline__ void hop_lam_halo(cx<R> (&acc)[V][12], const cx<R>* __restrict__ hp, int64_t hstride,
                                              const cx<R>* __restrict__ up, int64_t estride) {
   using C = cx<R>;
@@ -251,13 +252,14 @@ __device__ __forceinline__ void hop_lam_halo(cx<R> (&acc)[V][12], const cx<R>* _
 #pragma unroll
   for (int k = 0; k < 6; ++k) {
     C tmp[V];
-    VecIO<R, V>::ld(tmp, hp + k * hstride);
+    if constexpr (SS) VecIO<R, V>::lds(tmp, hp + k * hstride);
+    else VecIO<R, V>::ld(tmp, hp + k * hstride);
 #pragma unroll
     for (int v = 0; v < V; ++v) hh[v][k] = tmp[v];
   }
   C u[9];
 #pragma unroll
-  for (int e = 0; e < 9; ++e) u[e] = __ldg(up + e * estride);
+  for (int e = 0; e < 9; ++e) u[e] = SL ? up[e * estride] : __ldg(up + e * estride);
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     C h[2][3], g[2][3];
@@ -272,13 +274,14 @@ __device__ __forceinline__ void hop_lam_halo(cx<R> (&acc)[V][12], const cx<R>* _
 }
 
 // Backward T hop whose U^H-multiplied half spinor comes from the chi face.
-template <typename R, int V>
+template <typename R, int V, bool SS = false>
 __device__ __forceinline__ void hop_chi_halo(cx<R> (&acc)[V][12], const cx<R>* __restrict__ hp, int64_t hstride) {
   using C = cx<R>;
 #pragma unroll
   for (int k = 0; k < 6; ++k) {
     C tmp[V];
-    VecIO<R, V>::ld(tmp, hp + k * hstride);
+    if constexpr (SS) VecIO<R, V>::lds(tmp, hp + k * hstride);
+    else VecIO<R, V>::ld(tmp, hp + k * hstride);
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       // sign +1 reconstruction with A_0 = I: upper += g, lower -= g

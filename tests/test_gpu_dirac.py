@@ -152,32 +152,46 @@ def test_schur_constant_field_and_singular():
     assert "site" in str(err.value)
 
 
+HALO_SHAPES = [((8, 4, 4, 6), 3, "c128"),    # generic kernel
+               ((8, 4, 4, 16), 4, "c128"),   # ring kernel with halo tiles
+               ((8, 4, 4, 16), 12, "c128"),
+               ((8, 4, 4, 16), 16, "c64"),
+               ((8, 4, 4, 32), 8, "c64")]
+
+
 @pytest.mark.parametrize("nranks", [2, 4])
 @pytest.mark.parametrize("parity", [None, 0, 1])
-def test_tsplit_halo_kernels_reproduce_single_gpu(nranks, parity):
-    """Emulate the T split on one GPU: per-slab pack -> face swap -> hop with halos."""
+@pytest.mark.parametrize("shape", HALO_SHAPES, ids=lambda s: f"{s[0][3]}z_b{s[1]}_{s[2]}")
+@pytest.mark.parametrize("split_launch", [False, True], ids=["whole_slab", "interior_boundary"])
+def test_tsplit_halo_kernels_reproduce_single_gpu(nranks, parity, shape, split_launch):
+    """Emulate the T split on one GPU: per-slab pack -> face swap -> hop with
+    halos, either one launch over the slab or TSplitComm's sequence (interior
+    slices, then the two boundary slices); nrhs >= 4 runs the ring kernel with
+    the halo faces as bulk-copied tiles (the boundary fast path)."""
     import torch
     from paper_2601_05816_b200 import _lib
     from paper_2601_05816_b200.device import DeviceField, upload, upload_gauge
     from paper_2601_05816_b200.dirac import hop_device
     from paper_2601_05816_b200.oddeven import device_split
 
-    dims = (8, 4, 4, 6)
+    dims, b, dt = shape
     geom = P.LatticeGeometry(dims)
     links = O.flip_time_boundary(O.near_unit_gauge(dims, 0.3, 21), dims)
-    psi = O.gen_spinor(geom.n_sites, 3, 22)
+    psi = O.gen_spinor(geom.n_sites, b, 22)
     full_lat = _lib.Lattice.make(dims)
-    g_full = upload_gauge(P.GaugeField(geom, links))
-    d_psi = upload(host_field(psi, 2, geom))
+    g_full = upload_gauge(P.GaugeField(geom, links), dt)
+    d_psi = upload(host_field(psi, 2, geom), dt)
+    code = 0 if dt == "c128" else 1
+    tdt = torch.complex128 if dt == "c128" else torch.complex64
     if parity is None:
-        ref = DeviceField.empty(geom.n_sites, 3)
-        hop_device(full_lat, "c128", 3, -1, g_full, d_psi, ref, d_psi, 4.1, -1.0)
+        ref = DeviceField.empty(geom.n_sites, b, dtype=dt)
+        hop_device(full_lat, dt, b, -1, g_full, d_psi, ref, d_psi, 4.1, -1.0)
         src_full = d_psi
     else:
         e, o = device_split(full_lat, d_psi)
         src_full = o if parity == 0 else e  # source parity 1-p
-        ref = DeviceField.empty(geom.n_sites // 2, 3)
-        hop_device(full_lat, "c128", 3, parity, g_full, src_full, ref, None, 0.0, 1.0)
+        ref = DeviceField.empty(geom.n_sites // 2, b, dtype=dt)
+        hop_device(full_lat, dt, b, parity, g_full, src_full, ref, None, 0.0, 1.0)
     tl = dims[0] // nranks
     per_t = geom.sites_per_slice
     per = per_t if parity is None else per_t // 2
@@ -185,29 +199,33 @@ def test_tsplit_halo_kernels_reproduce_single_gpu(nranks, parity):
     for r in range(nranks):
         lg = P.LatticeGeometry((tl,) + dims[1:])
         lat = _lib.Lattice.make(lg.dims, r * tl)
-        gl = upload_gauge(P.GaugeField(lg, links[r * tl * per_t:(r + 1) * tl * per_t]))
+        gl = upload_gauge(P.GaugeField(lg, links[r * tl * per_t:(r + 1) * tl * per_t]), dt)
         nloc = tl * per
         src = DeviceField(src_full.data[r * nloc // 8:(r + 1) * nloc // 8].contiguous(), nloc)
-        lam = torch.empty((6, per, 3), dtype=torch.complex128, device="cuda")
+        lam = torch.empty((6, per, b), dtype=tdt, device="cuda")
         chi = torch.empty_like(lam)
         sp = -1 if parity is None else 1 - parity
-        _lib.call("b200wd_halo_pack", lat, 0, 3, sp, gl.ptr, src.ptr, lam.data_ptr(), chi.data_ptr(), 0)
+        _lib.call("b200wd_halo_pack", lat, code, b, sp, gl.ptr, src.ptr, lam.data_ptr(), chi.data_ptr(), 0)
         slabs.append((lg, lat, gl, src, lam, chi))
     outs = []
     for r, (lg, lat, gl, src, _, _) in enumerate(slabs):
         lam_from_up = slabs[(r + 1) % nranks][4]
         chi_from_down = slabs[(r - 1) % nranks][5]
         out = DeviceField(torch.empty_like(src.data), src.n)
-        if parity is None:
-            hop_device(lat, "c128", 3, -1, gl, src, out, src, 4.1, -1.0, lam_halo=lam_from_up,
-                       chi_halo=chi_from_down)
+        xs, al, be = (src, 4.1, -1.0) if parity is None else (None, 0.0, 1.0)
+        pp = -1 if parity is None else parity
+        if not split_launch:
+            hop_device(lat, dt, b, pp, gl, src, out, xs, al, be, lam_halo=lam_from_up, chi_halo=chi_from_down)
         else:
-            hop_device(lat, "c128", 3, parity, gl, src, out, None, 0.0, 1.0, lam_halo=lam_from_up,
-                       chi_halo=chi_from_down)
+            if tl > 2:
+                hop_device(lat, dt, b, pp, gl, src, out, xs, al, be, t_begin=1, t_end=tl - 1)
+            for t0, t1 in ((0, 1), (tl - 1, tl)):
+                hop_device(lat, dt, b, pp, gl, src, out, xs, al, be, t_begin=t0, t_end=t1, lam_halo=lam_from_up,
+                           chi_halo=chi_from_down)
         outs.append(out.data)
     got = torch.cat(outs, dim=0)
     err = (got - ref.data).abs().max().item() / ref.data.abs().max().item()
-    assert err < 1e-14
+    assert err < (1e-14 if dt == "c128" else 1e-6), err
 
 
 # ---- clover term (reference fixtures use random clover) ----
