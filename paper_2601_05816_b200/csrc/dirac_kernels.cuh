@@ -31,6 +31,18 @@ namespace b200wd {
 #ifndef B200WD_RING_NOMATH
 #define B200WD_RING_NOMATH 0  // experiment: consumers skip the t/x/y arithmetic
 #endif
+// Consumers hand a t/x/y tile back to the producer as soon as its data is in
+// registers (hop_load), then compute (hop_compute): the slot refills while the
+// FP64 work runs.  Measured (tools/sweep_dirac.py, 16^3x32; tools/time_apply.py
+// 48^3x96): c128 nrhs 16 0.564 -> 0.575, nrhs 32 0.485 -> 0.495, c64 nrhs 12
+// 0.467 -> 0.485, 48^3x96 c128 nrhs 12 21.9 -> 20.8 ms; c128 nrhs <= 8 lost
+// 3% (two hops of registers at 8 consumer warps), so it stays off there.
+// B200WD_RING_EARLY_RELEASE=0/1 forces it (variant builds).
+#ifdef B200WD_RING_EARLY_RELEASE
+template <typename R, int B> __host__ __device__ constexpr bool ring_early_release() { return B200WD_RING_EARLY_RELEASE != 0; }
+#else
+template <typename R, int B> __host__ __device__ constexpr bool ring_early_release() { return !(sizeof(R) == 8 && B <= 8); }
+#endif
 
 // Threads per block of the hopping kernel and the occupancy target handed
 // to ptxas (c128: <= 168 registers -> 3 blocks = 12 warps per SM; c64: 4 blocks).
@@ -606,16 +618,27 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
       hop_lam_halo<R, V, true, true>(acc, sb + (j * 8 + lo) * B + r0, NB * 8 * B, sb + Sh::SPIN + lofs, 8); \
     else if (HALO && (H) == 1 && item_t == 0)                                                        \
       hop_chi_halo<R, V, true>(acc, sb + (j * 8 + lo) * B + r0, NB * 8 * B);                         \
-    else if (!B200WD_RING_NOMATH)                                                                    \
+    else if (ring_early_release<R, B>()) {                                                           \
+      HopRegs<R, V> hr;                                                                              \
+      hop_load<((H) >> 1), !((H)&1), R, V, KST>(hr, sb + j * 96 * B + lo * B + r0, sb + Sh::SPIN + lofs); \
+      __syncwarp();                                                                                  \
+      if (lead) mbar_arrive(&empty[slot]);                                                           \
+      released = true;                                                                               \
+      hop_compute<((H) >> 1), !((H)&1), R, V>(acc, hr);                                              \
+    } else if (!B200WD_RING_NOMATH)                                                                  \
       hop_full<((H) >> 1), !((H)&1), R, V, true, true>(acc, sb + j * 96 * B + lo * B + r0, KST,      \
                                                         sb + Sh::SPIN + lofs, 8);                    \
-    __syncwarp();                                                                                    \
-    if (lead) mbar_arrive(&empty[slot]);                                                             \
+    if (!released) {                                                                                 \
+      __syncwarp();                                                                                  \
+      if (lead) mbar_arrive(&empty[slot]);                                                           \
+    }                                                                                                \
+    released = false;                                                                                \
     if (++cslot == S) {                                                                              \
       cslot = 0;                                                                                     \
       cphase ^= 1u;                                                                                  \
     }                                                                                                \
   }
+    bool released = false;
     B200WD_CONSUME(0)
     B200WD_CONSUME(1)
     B200WD_CONSUME(2)

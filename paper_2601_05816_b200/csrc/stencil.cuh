@@ -242,6 +242,44 @@ __device__ __forceinline__ void hop_full(cx<R> (&acc)[V][12], const cx<R>* __res
   }
 }
 
+// Split hop for early slot release: (1) hop_load reads the neighbour spinor
+// (projected 12 -> 6 as the components arrive) and the 9 link entries from
+// shared memory into registers -- after it the ring slot can be handed back
+// to the producer --, (2) hop_compute multiplies and reconstructs.
+template <typename R, int V> struct HopRegs {
+  cx<R> h[V][2][3];
+  cx<R> u[9];
+};
+template <int MU, bool FWD, typename R, int V, int KST>
+__device__ __forceinline__ void hop_load(HopRegs<R, V>& d, const cx<R>* sp, const cx<R>* up) {
+  using C = cx<R>;
+#pragma unroll
+  for (int S = 0; S < 2; ++S)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      C a[V], b[V];
+      VecIO<R, V>::lds(a, sp + (3 * S + c) * KST);
+      VecIO<R, V>::lds(b, sp + (6 + 3 * a_perm(MU, S) + c) * KST);
+      constexpr int code0 = FWD ? a_code(MU, 0) : ((a_code(MU, 0) + 2) & 3);
+      constexpr int code1 = FWD ? a_code(MU, 1) : ((a_code(MU, 1) + 2) & 3);
+#pragma unroll
+      for (int v = 0; v < V; ++v) d.h[v][S][c] = cadd(a[v], S == 0 ? phase<code0>(b[v]) : phase<code1>(b[v]));
+    }
+#pragma unroll
+  for (int e = 0; e < 9; ++e) d.u[e] = up[e * 8];
+}
+template <int MU, bool FWD, typename R, int V>
+__device__ __forceinline__ void hop_compute(cx<R> (&acc)[V][12], const HopRegs<R, V>& d) {
+  using C = cx<R>;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    C g[2][3];
+    matvec2<!FWD>(g, d.u, d.h[v]);
+    accumulate_spin<MU, FWD, 0>(acc[v], g);
+    accumulate_spin<MU, FWD, 1>(acc[v], g);
+  }
+}
+
 // Forward T hop whose projected half spinor comes from the lam halo face.
 // SS / SL: face / link in shared memory (the ring kernel's halo tiles).
 template <typename R, int V, bool SS = false, bool SL = false>
