@@ -816,9 +816,11 @@ static int* wave_counters(int64_t n, cudaStream_t st) {
 }
 
 // Wave synchronisation of a patched (TILED) traversal: one wave per patch
-// slice (B200WD_WAVE=0 turns it off, B200WD_WAVE_SLACK sets the slack).
+// slice (B200WD_WAVE=1 turns it on, B200WD_WAVE_SLACK sets the slack).  Off by
+// default: on the checkerboard Schur hops of 32^3 x 64 it cost 0.549 -> 0.484
+// of HBM (their patch slices are small, so the waits dominate).
 static void setup_waves(HopParams& p, int64_t n_items, int lz, cudaStream_t st) {
-  static const int en = ring_knob("B200WD_WAVE", 1);
+  static const int en = ring_knob("B200WD_WAVE", 0);
   static const int slack = ring_knob("B200WD_WAVE_SLACK", 2);
   p.wave_cnt = nullptr;
   if (!en || p.tile_x == 0) return;

@@ -30,7 +30,7 @@ def test_wave_synchronised_full_lattice_traversal_matches_oracle(kb):
     """The full-lattice patched order with wave synchronisation (used when a
     T slice exceeds the L2 reuse limit, e.g. 48^3 x 96) forced on a small
     lattice: B200WD_SLICE_KB lowers the limit, B200WD_WAVE_KB sizes the patch."""
-    env = dict(os.environ, B200WD_SLICE_KB="1", B200WD_WAVE_KB=kb, B200WD_TILE_KB=kb)
+    env = dict(os.environ, B200WD_SLICE_KB="1", B200WD_WAVE_KB=kb, B200WD_TILE_KB=kb, B200WD_WAVE="1")
     r = subprocess.run([sys.executable, str(ROOT / "tests" / "helpers" / "traversal_check.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
