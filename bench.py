@@ -51,7 +51,7 @@ M0 = 0.1
 METRIC = "D_W apply site*rhs/s (16^3x32, nrhs=16, c128)"
 
 
-PROFILE = ROOT / "profiles" / "r1_ncu_ring_c128_b16_cfg2_final.json"
+PROFILE = ROOT / "profiles" / "r2_ncu_ring_c128_b16_cfg2_final.json"
 
 
 def profile_traffic():
