@@ -336,3 +336,38 @@ def test_thread_transport_semantics_and_timeout():
     g = ThreadGroup(2)
     with pytest.raises(HaloTimeoutError, match="rank 0"):
         g.transport(0).allreduce(torch.zeros(1), timeout_s=0.2)
+
+
+def _timeout_worker(rank, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    from paper_2601_05816_b200.tsplit import DistTransport, HaloTimeoutError
+    tr = DistTransport()
+    bufs = [torch.zeros(4) for _ in range(4)]
+    if rank == 1:  # a rank that never posts its faces (hung / dead peer)
+        import time
+        time.sleep(6)
+        q.put((rank, "silent"))
+        return
+    try:
+        tr.wait(tr.exchange(*bufs, 1, 1), 1.5, rank)
+        q.put((rank, "completed"))
+    except HaloTimeoutError as e:
+        q.put((rank, f"HaloTimeoutError rank={e.rank} direction={e.direction}"))
+
+
+def test_dist_transport_raises_halo_timeout_naming_rank_and_direction():
+    """halo.py:43-53, 91-98: a receive that does not complete in time raises
+    HaloTimeoutError naming the waiting rank and the neighbour direction."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_timeout_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=20)
+        if p.is_alive():
+            p.kill()
+    assert res[0] == "HaloTimeoutError rank=0 direction=up", res
