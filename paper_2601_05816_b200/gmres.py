@@ -349,13 +349,16 @@ def solve_dirac(params: DiracParams, gauge, clover, eta, cfg: GmresConfig, odd_e
     if comm is not None:
         return comm.solve_dirac(params, gauge, clover, eta, cfg, odd_even=odd_even, psi0=psi0)
     d_eta = upload(eta, "c128") if host else eta
+    # the links (and clover) cross PCIe once per solve: both operators share the device copy
+    from .device import gauge_cache
+    gauge = gauge_cache.get(gauge, "c128")
     dirac = DiracOperator(params, gauge, clover, "c128")
     if not odd_even:
         res = gmres_solve(dirac, d_eta, psi0, cfg)
         psi = res.psi
         full = res.final_relnorms
     else:
-        schur = SchurOperator(params, gauge, clover, dtype="c128")
+        schur = SchurOperator(params, gauge, clover, dtype="c128", gauge_dev=gauge)
         reduced, eta_elim = schur.reduce_rhs(d_eta)
         x0 = None
         if psi0 is not None:

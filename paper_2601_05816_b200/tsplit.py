@@ -386,6 +386,7 @@ class TSplitComm:
         from .oddeven import device_split
         host = not isinstance(eta, DeviceField)
         d_eta = upload(eta, "c128") if host else eta
+        gauge = gauge_cache.get(gauge, "c128")  # one upload of this rank's links per solve
         op = self.operator(params, gauge, clover, "c128")
         if not odd_even:
             res = gmres_solve(op, d_eta, psi0, cfg)
