@@ -134,6 +134,14 @@ int b200wd_hop_clover(const b200wd_lattice* lat, int32_t dtype, int32_t b, int32
                       double beta, const double* scale, int32_t t_begin, int32_t t_end,
                       const void* lam_halo, const void* chi_halo, const void* clover,
                       int32_t clover_mode, void* stream);
+/* Both T-split boundary slices (local slices 0 and T-1) consuming the halo
+ * faces in ONE launch (halo.py:370-387): the same arithmetic as two
+ * b200wd_hop(_clover) calls with t ranges [0,1) and [T-1,T); clover may be
+ * NULL (clover_mode 0). */
+int b200wd_hop_boundary(const b200wd_lattice* lat, int32_t dtype, int32_t b, int32_t dst_parity,
+                        const void* links, const void* src, const void* xself, void* out, double alpha,
+                        double beta, const double* scale, const void* lam_halo, const void* chi_halo,
+                        const void* clover, int32_t clover_mode, void* stream);
 /* out = M x, site-local (D_oo^-1 eta_o of reduce_rhs, oddeven.py:179-188). */
 int b200wd_clover_apply(int64_t n_sites, int32_t dtype, int32_t b, const void* blocks,
                         const void* x, void* out, void* stream);

@@ -107,6 +107,7 @@ SIGNATURES = {
     "b200wd_dirac_apply": [_LAT, _i32, _i32, _dbl, _vp, _vp, _vp, _vp],
     "b200wd_hop_clover": [_LAT, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _dbl, _dbl, _vp, _i32, _i32, _vp, _vp, _vp,
                           _i32, _vp],
+    "b200wd_hop_boundary": [_LAT, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _dbl, _dbl, _vp, _vp, _vp, _vp, _i32, _vp],
     "b200wd_clover_apply": [_i64, _i32, _i32, _vp, _vp, _vp, _vp],
     "b200wd_clover_import": [_vp, _i64, _vp, _i32, _vp],
     "b200wd_halo_pack": [_LAT, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp],

@@ -122,6 +122,40 @@ extern "C" int b200wd_hop_clover(const b200wd_lattice* lat, int32_t dtype, int32
   return check_launch("b200wd_hop_clover");
 }
 
+extern "C" int b200wd_hop_boundary(const b200wd_lattice* lat, int32_t dtype, int32_t b, int32_t dst_parity,
+                                   const void* links, const void* src, const void* xself, void* out, double alpha,
+                                   double beta, const double* scale, const void* lam_halo, const void* chi_halo,
+                                   const void* clover, int32_t clover_mode, void* stream) {
+  HopParams p;
+  if (int rc = fill_params(p, lat, dtype, b, dst_parity)) return rc;
+  B200WD_REQUIRE(links && src && out, "NULL field pointer");
+  B200WD_REQUIRE(lam_halo && chi_halo, "the boundary slices need both halo faces");
+  B200WD_REQUIRE(clover_mode >= 0 && clover_mode <= 2, "clover_mode must be 0, 1 or 2 (got %d)", clover_mode);
+  B200WD_REQUIRE(clover_mode == 0 || clover != nullptr, "clover_mode %d needs a clover array", clover_mode);
+  p.U = links;
+  p.src = src;
+  p.xself = xself;
+  p.out = out;
+  p.alpha = alpha;
+  p.beta = 0.5 * beta;
+  p.scale = scale;
+  p.lam_halo = lam_halo;
+  p.chi_halo = chi_halo;
+  p.clov = clover;
+  p.clov_mode = clover_mode;
+  const int64_t per = dst_parity < 0 ? p.per_t : p.per_t / 2;
+  p.d_begin = 0;
+  p.d_end = 2 * per;  // slice 0 and slice T-1 (contiguous when T == 2)
+  if (p.T > 2) {
+    p.jump_at = per;
+    p.jump_by = (int64_t)(p.T - 2) * per;
+  }
+  cudaStream_t st = as_stream(stream);
+  if (dtype == B200WD_C128) launch_hop_c128(p, st);
+  else launch_hop_c64(p, st);
+  return check_launch("b200wd_hop_boundary");
+}
+
 extern "C" int b200wd_clover_apply(int64_t n_sites, int32_t dtype, int32_t b, const void* blocks, const void* x,
                                    void* out, void* stream) {
   B200WD_REQUIRE(n_sites >= 8 && n_sites % 8 == 0, "site count %lld must be a positive multiple of 8",

@@ -68,8 +68,9 @@ template <typename R, int V, int B>
 __global__ void __launch_bounds__(kHopThreads, HopMinBlocks<R, B>::value) hop_kernel(const HopParams p) {
   using C = cx<R>;
   if (hop_stopped(p)) return;
-  const int64_t d = p.d_begin + (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
+  int64_t d = p.d_begin + (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
   if (d >= p.d_end) return;
+  if (p.jump_by && d >= p.d_begin + p.jump_at) d += p.jump_by;  // two boundary slices in one launch
   const int b = B > 0 ? B : p.b;
   const int r0 = threadIdx.x * V;
   const int Z = p.Z, Y = p.Y, X = p.X, T = p.T;
@@ -439,7 +440,8 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
       bool sync = TILED && p.wave_cnt != nullptr;
       for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
         if (TILED && sync) sync = wave_wait(p, it, n_items);
-        const int64_t gb0 = (p.d_begin >> 3) + (TILED ? item_nat(it, p, lz) : it) * NB;
+        int64_t gb0 = (p.d_begin >> 3) + (TILED ? item_nat(it, p, lz) : it) * NB;
+        if (HALO && p.jump_by && gb0 * 8 >= p.d_begin + p.jump_at) gb0 += p.jump_by >> 3;
         const BlkCoord c0 = block_coord(gb0 * 8 * F, p);
 #if B200WD_L2_PREFETCH
         {  // warm L2 with the compulsory misses of a later item of this CTA:
@@ -518,7 +520,8 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
   for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
     // natural order keeps gb0 affine in `it`: a separate instantiation,
     // the compiler schedules that loop markedly better (tools/bench_strong.py)
-    const int64_t gb0 = (p.d_begin >> 3) + (TILED ? item_nat(it, p, lz) : it) * NB;
+    int64_t gb0 = (p.d_begin >> 3) + (TILED ? item_nat(it, p, lz) : it) * NB;
+    if (HALO && p.jump_by && gb0 * 8 >= p.d_begin + p.jump_at) gb0 += p.jump_by >> 3;
     const int64_t d = (gb0 + j) * 8 + lo;  // field index of this thread's site
     // natural site: full lattice d; checkerboard 2d + (parity fix of the block's line)
     int64_t xn = d;
@@ -885,6 +888,7 @@ static bool launch_ring_nb(const HopParams& p_in, int64_t nblk, int S, cudaStrea
     return false;
   } else {
     if (nblk % NB) return false;
+    if (p_in.jump_by && ((p_in.jump_at >> 3) % NB)) return false;  // items must not straddle the jump
     HopParams p = p_in;
     const size_t site_bytes = (size_t)12 * B * sizeof(cx<R>);
     // patched order for checkerboard fields only: measured +2-8% on the Schur

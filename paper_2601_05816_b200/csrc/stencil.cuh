@@ -64,6 +64,10 @@ struct HopParams {
   int* wave_cnt;
   int64_t wave_items;
   int32_t wave_slack;
+  // both T-split boundary slices in one launch: destination field indices
+  // d >= d_begin + jump_at are shifted by jump_by (skipping the interior
+  // slices); the range [d_begin, d_end) counts the two slices only.  0: off
+  int64_t jump_at, jump_by;
 };
 
 // bounded wait until wave w-slack is complete; false once a wait timed out

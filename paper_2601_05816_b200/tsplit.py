@@ -81,6 +81,13 @@ class CudaHaloKernels:
                   None if xself is None else xself.ptr, out.ptr, float(alpha), float(beta), ptr(scale), int(t0),
                   int(t1), ptr(lam), ptr(chi), stream_ptr())
 
+    def hop_boundary(self, lat, dtype, b, dst_parity, gauge, src, out, xself, alpha, beta, scale, lam, chi,
+                     clover=None, mode=0):
+        """Both boundary slices (0 and T-1) with their halos in one launch."""
+        _lib.call("b200wd_hop_boundary", lat, dtype_code(dtype), b, dst_parity, gauge.ptr, src.ptr,
+                  None if xself is None else xself.ptr, out.ptr, float(alpha), float(beta), ptr(scale), ptr(lam),
+                  ptr(chi), None if clover is None else clover.ptr, int(mode), stream_ptr())
+
     def face_buffer(self, nf, b, dtype, device):
         t = torch.complex128 if dtype == "c128" else torch.complex64
         return torch.empty((6, nf, b), dtype=t, device=device)
@@ -290,9 +297,12 @@ class TSplitComm:
         self.stats["wait_s"] += time.perf_counter() - t_w
         if ev:
             ev[2].record()
-        # both boundary slices in one launch when they are the whole slab (T = 2),
-        # else one launch each
-        if T == 2:
+        # both boundary slices in one launch (b200wd_hop_boundary); kernels
+        # without it (test stand-ins) take one launch per slice
+        if hasattr(k, "hop_boundary"):
+            k.hop_boundary(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, f["lam_in"],
+                           f["chi_in"], **extra)
+        elif T == 2:
             k.hop(self.lat, dtype, b, par, gauge, src, out, xself, alpha, beta, scale, 0, 2, f["lam_in"],
                   f["chi_in"], **extra)
         else:
@@ -306,8 +316,8 @@ class TSplitComm:
             self.stats["interior_ms"] += ev[0].elapsed_time(ev[1])
             self.stats["boundary_ms"] += ev[2].elapsed_time(ev[3])
         self.stats["applies"] += 1
-        # pack + interior (T > 2) + boundary slices (one launch when T == 2)
-        self.stats["launches"] += 1 + (1 if T > 2 else 0) + (1 if T == 2 else 2)
+        # pack + interior (T > 2) + boundary slices (one launch with hop_boundary)
+        self.stats["launches"] += 1 + (1 if T > 2 else 0) + (1 if (T == 2 or hasattr(k, "hop_boundary")) else 2)
         return out
 
     def _events(self):

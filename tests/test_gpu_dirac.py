@@ -162,7 +162,7 @@ HALO_SHAPES = [((8, 4, 4, 6), 3, "c128"),    # generic kernel
 @pytest.mark.parametrize("nranks", [2, 4])
 @pytest.mark.parametrize("parity", [None, 0, 1])
 @pytest.mark.parametrize("shape", HALO_SHAPES, ids=lambda s: f"{s[0][3]}z_b{s[1]}_{s[2]}")
-@pytest.mark.parametrize("split_launch", [False, True], ids=["whole_slab", "interior_boundary"])
+@pytest.mark.parametrize("split_launch", [0, 1, 2], ids=["whole_slab", "interior_boundary", "boundary_merged"])
 def test_tsplit_halo_kernels_reproduce_single_gpu(nranks, parity, shape, split_launch):
     """Emulate the T split on one GPU: per-slab pack -> face swap -> hop with
     halos, either one launch over the slab or TSplitComm's sequence (interior
@@ -219,9 +219,14 @@ def test_tsplit_halo_kernels_reproduce_single_gpu(nranks, parity, shape, split_l
         else:
             if tl > 2:
                 hop_device(lat, dt, b, pp, gl, src, out, xs, al, be, t_begin=1, t_end=tl - 1)
-            for t0, t1 in ((0, 1), (tl - 1, tl)):
-                hop_device(lat, dt, b, pp, gl, src, out, xs, al, be, t_begin=t0, t_end=t1, lam_halo=lam_from_up,
-                           chi_halo=chi_from_down)
+            if split_launch == 1:
+                for t0, t1 in ((0, 1), (tl - 1, tl)):
+                    hop_device(lat, dt, b, pp, gl, src, out, xs, al, be, t_begin=t0, t_end=t1,
+                               lam_halo=lam_from_up, chi_halo=chi_from_down)
+            else:  # both boundary slices in one launch (b200wd_hop_boundary)
+                _lib.call("b200wd_hop_boundary", lat, code, b, pp, gl.ptr, src.ptr,
+                          None if xs is None else xs.ptr, out.ptr, al, be, None, lam_from_up.data_ptr(),
+                          chi_from_down.data_ptr(), None, 0, 0)
         outs.append(out.data)
     got = torch.cat(outs, dim=0)
     err = (got - ref.data).abs().max().item() / ref.data.abs().max().item()

@@ -46,9 +46,8 @@ for dt in a.dtypes:
                   None)
         _lib.call("b200wd_hop", lat, code, b, -1, U.data_ptr(), x.data_ptr(), x.data_ptr(), y.data_ptr(), 4.1, -1.0,
                   None, 1, T - 1, None, None, None)
-        for t0, t1 in ((0, 1), (T - 1, T)):
-            _lib.call("b200wd_hop", lat, code, b, -1, U.data_ptr(), x.data_ptr(), x.data_ptr(), y.data_ptr(), 4.1,
-                      -1.0, None, t0, t1, lam.data_ptr(), chi.data_ptr(), None)
+        _lib.call("b200wd_hop_boundary", lat, code, b, -1, U.data_ptr(), x.data_ptr(), x.data_ptr(), y.data_ptr(),
+                  4.1, -1.0, None, lam.data_ptr(), chi.data_ptr(), None, 0, None)
 
     def timed(fn):
         for _ in range(3):
@@ -66,13 +65,14 @@ for dt in a.dtypes:
     # pieces of the split
     ti = timed(lambda: _lib.call("b200wd_hop", lat, code, b, -1, U.data_ptr(), x.data_ptr(), x.data_ptr(),
                                  y.data_ptr(), 4.1, -1.0, None, 1, T - 1, None, None, None))
-    tb = timed(lambda: [_lib.call("b200wd_hop", lat, code, b, -1, U.data_ptr(), x.data_ptr(), x.data_ptr(),
+    tb = timed(lambda: _lib.call("b200wd_hop_boundary", lat, code, b, -1, U.data_ptr(), x.data_ptr(), x.data_ptr(), y.data_ptr(), 4.1, -1.0, None, lam.data_ptr(), chi.data_ptr(), None, 0, None))
+    tb2 = timed(lambda: [_lib.call("b200wd_hop", lat, code, b, -1, U.data_ptr(), x.data_ptr(), x.data_ptr(),
                                   y.data_ptr(), 4.1, -1.0, None, t0, t1, lam.data_ptr(), chi.data_ptr(), None)
                         for t0, t1 in ((0, 1), (T - 1, T))])
     tp = timed(lambda: _lib.call("b200wd_halo_pack", lat, code, b, -1, U.data_ptr(), x.data_ptr(), lam.data_ptr(),
                                  chi.data_ptr(), None))
     print(json.dumps({"dims": a.dims, "dtype": dt, "b": b, "full_ms": round(tf, 4), "split_ms": round(ts, 4),
-                      "overhead": round(ts / tf - 1, 4), "interior_ms": round(ti, 4), "boundary_ms": round(tb, 4),
+                      "overhead": round(ts / tf - 1, 4), "interior_ms": round(ti, 4), "boundary_ms": round(tb, 4), "boundary_two_launches_ms": round(tb2, 4),
                       "pack_ms": round(tp, 4),
                       "boundary_per_slice_vs_full_per_slice": round((tb / 2) / (tf / T), 3)}), flush=True)
     del U, x, y, lam, chi
