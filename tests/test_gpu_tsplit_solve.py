@@ -122,3 +122,51 @@ def test_split_solve_stats_record_wait_and_hops():
     reps, _, stats = _solve_split(g, 2, True, timing=True)
     for s in stats:
         assert s["applies"] > 0 and s["interior_ms"] > 0 and s["boundary_ms"] > 0 and s["wait_s"] >= 0
+
+
+@pytest.mark.parametrize("odd_even", [False, True])
+def test_split_solve_with_clover_matches_single_gpu(odd_even):
+    """The clover term rides in every interior and boundary hop of the split
+    (b200wd_hop_clover / b200wd_hop_boundary): thread-rank solves at world 2
+    and 4 agree with the single-GPU solve (reference fixtures use clover)."""
+    import torch
+
+    from paper_2601_05816_b200.tsplit import ThreadGroup, TSplitComm
+    dims = (16, 4, 4, 8)
+    geom = P.LatticeGeometry(dims)
+    links = O.flip_time_boundary(O.near_unit_gauge(dims, 0.3, 31), dims)
+    packed = O.pack_clover(O.gen_clover_random(dims, 0.05, 32))
+    eta = O.gen_spinor(geom.n_sites, 4, 33)
+    cfg = P.GmresConfig(restart_len=12, restarts=40, tol=1e-9)
+    ref = P.solve_dirac(P.DiracParams(m0=0.1), P.GaugeField(geom, links), P.CloverField(geom, packed),
+                        _host_field(eta, geom), cfg, odd_even=odd_even)
+    per_t = geom.sites_per_slice
+    for world in (2, 4):
+        grp = ThreadGroup(world)
+        reps, errs = [None] * world, []
+
+        def rank_main(r):
+            try:
+                torch.cuda.set_device(0)
+                comm = TSplitComm(geom, transport=grp.transport(r))
+                lg, t0 = comm.local_geom, comm.t_origin
+                sl = slice(t0 * per_t, (t0 + lg.dims[0]) * per_t)
+                reps[r] = comm.solve_dirac(P.DiracParams(m0=0.1), P.GaugeField(lg, links[sl]),
+                                           P.CloverField(lg, packed[sl]), _host_field(eta[sl], lg), cfg,
+                                           odd_even=odd_even)
+            except BaseException as e:  # noqa: BLE001
+                errs.append(e)
+                grp.barrier.abort()
+
+        th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=600)
+        if errs:
+            raise errs[0]
+        assert abs(reps[0].iterations - ref.iterations) <= 1, (world, reps[0].iterations, ref.iterations)
+        psi = np.concatenate([rp.psi.ksi() for rp in reps])
+        err = np.linalg.norm(psi - ref.psi.ksi()) / np.linalg.norm(ref.psi.ksi())
+        assert err < 1e-8, (world, err)
+        assert all(np.all(np.asarray(rp.full_relnorms) <= 1e-9) for rp in reps)
