@@ -39,7 +39,10 @@ def needs_build() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: Path | None = None) -> Path:
+def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: Path | None = None,
+          only: tuple = ()) -> Path:
+    """only: (variant builds) translation units compiled with `defines`; the
+    others are taken from the default build's objects."""
     lib = Path(out) if out else LIB
     if not force and out is None and not needs_build():
         return LIB
@@ -50,6 +53,9 @@ def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: 
     procs = []
     for src in SOURCES:  # translation units compile in parallel
         obj = tmp / (Path(src).stem + ".o")
+        if only and Path(src).stem not in only:
+            objs.append(str(PKG / "build" / "default" / (Path(src).stem + ".o")))
+            continue
         cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(ROOT / "include"), "-I", str(CSRC),
                "-c", str(CSRC / src), "-o", str(obj)]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
@@ -74,4 +80,6 @@ def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: 
 if __name__ == "__main__":
     defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))
     outs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
-    print(build(force="--force" in sys.argv, verbose=True, defines=defs, out=Path(outs[0]) if outs else None))
+    only = tuple(x for a in sys.argv[1:] if a.startswith("--only=") for x in a.split("=", 1)[1].split(","))
+    print(build(force="--force" in sys.argv, verbose="--quiet" not in sys.argv, defines=defs,
+                out=Path(outs[0]) if outs else None, only=only))

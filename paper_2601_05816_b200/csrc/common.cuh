@@ -167,6 +167,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// 16-byte LDGSTS copy global -> shared (L1-bypassing) and its completion as an
+// arrival on an mbarrier: the arrive fires once every earlier cp.async of the
+// executing thread has landed and takes one of the barrier's expected arrivals
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // L2 eviction-priority policies for the bulk copies (createpolicy)
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t pol;

@@ -31,6 +31,24 @@ namespace b200wd {
 #ifndef B200WD_RING_NOMATH
 #define B200WD_RING_NOMATH 0  // experiment: consumers skip the t/x/y arithmetic
 #endif
+// Experiment builds (timing only, results are wrong): bit 0 consumers only wait
+// for and release every tile (no LDS, no arithmetic), bit 1 no link copies,
+// bit 2 no t+1 / t-1 tiles, bit 3 consumers prefetch the t+1 blocks of a later
+// item into L2 (valid results), bit 4 no output stores.
+#ifndef B200WD_RING_EXP
+#define B200WD_RING_EXP 0
+#endif
+// Link planes of a tile through the producer warp's 32 lanes (cp.async /
+// LDGSTS, completion as mbarrier arrivals) instead of a second bulk copy per
+// tile: the bulk-copy engine handles ~4.9 M copies/s per SM whatever their
+// size (tools/mb_ingress.cu), and half of the ring's copies were 1-2 KB link
+// planes.
+#ifndef B200WD_LINK_LDGSTS
+#define B200WD_LINK_LDGSTS 1
+#endif
+#ifndef B200WD_RING_PFD
+#define B200WD_RING_PFD 1  // bit 3: items of this CTA ahead
+#endif
 // Consumers hand a t/x/y tile back to the producer as soon as its data is in
 // registers (hop_load), then compute (hop_compute): the slot refills while the
 // FP64 work runs.  Measured (tools/sweep_dirac.py, 16^3x32; tools/time_apply.py
@@ -321,10 +339,12 @@ __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, cons
   const C* src = static_cast<const C*>(p.src);
   const C* U = static_cast<const C*>(p.U);
   const int64_t nblk = p.n >> 3;  // natural link blocks
+  constexpr bool kLinks = !(B200WD_RING_EXP & 2) && !B200WD_LINK_LDGSTS;
+  constexpr int kSlotTx = kLinks ? Sh::SLOT : Sh::SPIN;
   if constexpr (H == 6) {
-    mbar_expect_tx(full, (uint32_t)(Sh::SLOT * sizeof(C)));
+    mbar_expect_tx(full, (uint32_t)(kSlotTx * sizeof(C)));
     bulk_g2s(slot, src + gb0 * 96 * B, Sh::SPIN * sizeof(C), full);
-    bulk_g2s(slot + Sh::SPIN, U + (3 * nblk + F * gb0) * 72, NB * Sh::LPB * sizeof(C), full);
+    if (kLinks) bulk_g2s(slot + Sh::SPIN, U + (3 * nblk + F * gb0) * 72, NB * Sh::LPB * sizeof(C), full);
   } else {
     constexpr int MU = H >> 1;
     constexpr bool FWD = !(H & 1);
@@ -338,16 +358,16 @@ __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, cons
         const C* fp = static_cast<const C*>(face);
         const int64_t i0 = gb0 * 8 - (int64_t)c0.t * (p.per_t / F);  // face index of the item's first field site
         constexpr int RUN = NB * 8 * B;
-        mbar_expect_tx(full, (uint32_t)((6 * RUN + NB * Sh::LPB) * sizeof(C)));
+        mbar_expect_tx(full, (uint32_t)((6 * RUN + (kLinks ? NB * Sh::LPB : 0)) * sizeof(C)));
 #pragma unroll
         for (int k = 0; k < 6; ++k) bulk_g2s(slot + k * RUN, fp + (k * p.nf + i0) * B, RUN * sizeof(C), full);
         // U_0 of the own blocks (the lam hop multiplies at the destination; unused by chi)
-        bulk_g2s(slot + Sh::SPIN, U + (0 * nblk + F * gb0) * 72, NB * Sh::LPB * sizeof(C), full);
+        if (kLinks) bulk_g2s(slot + Sh::SPIN, U + (0 * nblk + F * gb0) * 72, NB * Sh::LPB * sizeof(C), full);
         return;
       }
     }
     // neighbour field blocks of the NB own blocks: contiguous unless a wrap falls inside the item
-    mbar_expect_tx(full, (uint32_t)(Sh::SLOT * sizeof(C)));
+    mbar_expect_tx(full, (uint32_t)(kSlotTx * sizeof(C)));
     const int64_t nb0 = block_neighbor<MU, FWD>(gb0 * 8 * F, c0, p) / (8 * F);
     bool contiguous = true;
     if constexpr (NB > 1) {
@@ -365,7 +385,8 @@ __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, cons
         bulk_g2s_hint(slot, src + nb0 * 96 * B, Sh::SPIN * sizeof(C), full, pol_t1);
       else
         bulk_g2s(slot, src + nb0 * 96 * B, Sh::SPIN * sizeof(C), full);
-      bulk_g2s(slot + Sh::SPIN, U + (MU * nblk + F * (FWD ? gb0 : nb0)) * 72, NB * Sh::LPB * sizeof(C), full);
+      if (kLinks)
+        bulk_g2s(slot + Sh::SPIN, U + (MU * nblk + F * (FWD ? gb0 : nb0)) * 72, NB * Sh::LPB * sizeof(C), full);
     } else {
       BlkCoord c = c0;
 #pragma unroll
@@ -373,11 +394,52 @@ __device__ __forceinline__ void ring_issue(const HopParams& p, int64_t gb0, cons
         if (jj) block_step<F>(c, p);
         const int64_t nb = block_neighbor<MU, FWD>((gb0 + jj) * 8 * F, c, p) / (8 * F);
         bulk_g2s(slot + jj * 96 * B, src + nb * 96 * B, 96 * B * sizeof(C), full);
-        bulk_g2s(slot + Sh::SPIN + jj * Sh::LPB, U + (MU * nblk + F * (FWD ? gb0 + jj : nb)) * 72,
-                 Sh::LPB * sizeof(C), full);
+        if (kLinks)
+          bulk_g2s(slot + Sh::SPIN + jj * Sh::LPB, U + (MU * nblk + F * (FWD ? gb0 + jj : nb)) * 72,
+                   Sh::LPB * sizeof(C), full);
       }
     }
   }
+}
+
+// The link plane of tile H by the 32 lanes of the producer warp: 16-byte
+// cp.async copies, then one mbarrier arrival per lane (the full barrier expects
+// 1 + 32 arrivals per phase).  Same source runs as the bulk copies of ring_issue.
+template <typename R, int V, int B, int NB, bool PAR, int H, bool HALO = false>
+__device__ __forceinline__ void ring_issue_links(const HopParams& p, int64_t gb0, const BlkCoord& c0, cx<R>* slot,
+                                                 uint64_t* full, int lane) {
+  using C = cx<R>;
+  using Sh = RingShape<R, V, B, NB, PAR>;
+  constexpr int F = Sh::F;
+  constexpr int CH = 16 / (int)sizeof(C);  // complex per 16-byte chunk
+  const C* U = static_cast<const C*>(p.U);
+  const int64_t nblk = p.n >> 3;
+  C* dst = slot + Sh::SPIN;
+  auto run = [&](C* d, const C* s, int n_cx) {
+    for (int i = lane * CH; i < n_cx; i += 32 * CH) cp_async16(d + i, s + i);
+  };
+  if constexpr (H == 6) {
+    run(dst, U + (3 * nblk + F * gb0) * 72, NB * Sh::LPB);
+  } else {
+    constexpr int MU = H >> 1;
+    constexpr bool FWD = !(H & 1);
+    bool face = false;
+    if constexpr (HALO && H <= 1) face = H == 0 ? (c0.t + 1 == p.T) : (c0.t == 0);
+    if (face) {
+      run(dst, U + (0 * nblk + F * gb0) * 72, NB * Sh::LPB);
+    } else if constexpr (FWD) {
+      run(dst, U + (MU * nblk + F * gb0) * 72, NB * Sh::LPB);  // own blocks: one run
+    } else {
+      BlkCoord c = c0;
+#pragma unroll
+      for (int jj = 0; jj < NB; ++jj) {
+        if (jj) block_step<F>(c, p);
+        const int64_t nb = block_neighbor<MU, FWD>((gb0 + jj) * 8 * F, c, p) / (8 * F);
+        run(dst + jj * Sh::LPB, U + (MU * nblk + F * nb) * 72, Sh::LPB);
+      }
+    }
+  }
+  cp_async_mbar_arrive(full);
 }
 
 // TILED: patched traversal order (checkerboard fields).  ZG: items are not
@@ -413,7 +475,7 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
   const int tid = threadIdx.x;  // 1-D block: consumers [0, NC), producer warp [NC, NC+32)
   if (tid == 0) {
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], 1);
+      mbar_init(&full[i], B200WD_LINK_LDGSTS ? 33 : 1);
       mbar_init(&empty[i], Sh::NCW);
     }
     if constexpr (CLOV) {
@@ -427,7 +489,9 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
   __syncthreads();
 
   if (tid >= Sh::NC) {
-    if (tid == Sh::NC) {  // one elected lane issues every copy
+    const int lane = tid - Sh::NC;
+    // lane 0 issues every bulk copy; with B200WD_LINK_LDGSTS all 32 lanes copy the link planes
+    if (lane == 0 || B200WD_LINK_LDGSTS) {
       int pslot = 0, pfirst = 1;
       const uint64_t pol_first = l2_evict_first_policy();
       // t+1 blocks come back as own blocks one patch slice later (tiled) or
@@ -439,12 +503,15 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
       const uint32_t lz = (uint32_t)(p.Z / (8 * F * NB));
       bool sync = TILED && p.wave_cnt != nullptr;
       for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
-        if (TILED && sync) sync = wave_wait(p, it, n_items);
+        if (TILED && p.wave_cnt != nullptr) {
+          if (lane == 0 && sync) sync = wave_wait(p, it, n_items);
+          if (B200WD_LINK_LDGSTS) __syncwarp();
+        }
         int64_t gb0 = (p.d_begin >> 3) + (TILED ? item_nat(it, p, lz) : it) * NB;
         if (HALO && p.jump_by && gb0 * 8 >= p.d_begin + p.jump_at) gb0 += p.jump_by >> 3;
         const BlkCoord c0 = block_coord(gb0 * 8 * F, p);
 #if B200WD_L2_PREFETCH
-        {  // warm L2 with the compulsory misses of a later item of this CTA:
+        if (lane == 0) {  // warm L2 with the compulsory misses of a later item of this CTA:
            // its t+1 neighbour blocks (first touch in sweep order) and links
           const int64_t nx = it + (int64_t)B200WD_L2_PREFETCH * gridDim.x;
           if (nx < n_items) {
@@ -462,8 +529,16 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
 #endif
 #define B200WD_PRODUCE(H)                                                                   \
   {                                                                                         \
-    if (pfirst == 0) mbar_wait(&empty[pslot], pphase ^ 1u);                                 \
-    ring_issue<R, V, B, NB, PAR, H, HALO>(p, gb0, c0, ring + pslot * Sh::SLOT, &full[pslot], pol_first, pol_t1); \
+    if (pfirst == 0) {                                                                      \
+      if (lane == 0) mbar_wait(&empty[pslot], pphase ^ 1u);                                 \
+      if (B200WD_LINK_LDGSTS) __syncwarp();                                                 \
+    }                                                                                       \
+    if (lane == 0)                                                                          \
+      ring_issue<R, V, B, NB, PAR, H, HALO>(p, gb0, c0, ring + pslot * Sh::SLOT, &full[pslot], pol_first, pol_t1); \
+    if (B200WD_LINK_LDGSTS && !(B200WD_RING_EXP & 2))                                       \
+      ring_issue_links<R, V, B, NB, PAR, H, HALO>(p, gb0, c0, ring + pslot * Sh::SLOT, &full[pslot], lane); \
+    else if (B200WD_LINK_LDGSTS)                                                            \
+      cp_async_mbar_arrive(&full[pslot]);                                                   \
     if (++pslot == S) {                                                                     \
       pslot = 0;                                                                            \
       pphase ^= 1u;                                                                         \
@@ -471,7 +546,7 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
     }                                                                                       \
   }
         B200WD_PRODUCE(6)
-        if constexpr (CLOV) {  // this item's blocks (read in the epilogue)
+        if (CLOV && lane == 0) {  // this item's blocks (read in the epilogue)
           if (cb_first == 0) mbar_wait(&cempty[cb_slot], cb_phase ^ 1u);
           constexpr uint32_t cbytes = (uint32_t)(clov_tile<R, NB>() * sizeof(C));
           mbar_expect_tx(&cfull[cb_slot], cbytes);
@@ -483,14 +558,16 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
             cb_first = 0;
           }
         }
-        B200WD_PRODUCE(0)
-        B200WD_PRODUCE(1)
+        if (!(B200WD_RING_EXP & 4)) {
+          B200WD_PRODUCE(0)
+          B200WD_PRODUCE(1)
+        }
         B200WD_PRODUCE(2)
         B200WD_PRODUCE(3)
         B200WD_PRODUCE(4)
         B200WD_PRODUCE(5)
 #undef B200WD_PRODUCE
-        if (TILED && p.wave_cnt != nullptr) wave_arrive(p, it);
+        if (TILED && p.wave_cnt != nullptr && lane == 0) wave_arrive(p, it);
       }
     }
     return;
@@ -539,6 +616,26 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
       const int slot = cslot;
       mbar_wait(&full[slot], cphase);
       const C* zt = ring + slot * Sh::SLOT;
+      if constexpr ((B200WD_RING_EXP & 8) != 0) {
+        // first touch of the sweep: the t+1 blocks of a later item of this CTA,
+        // requested into L2 by the consumer threads (one 128-byte line each)
+        const int64_t nx = it + (int64_t)B200WD_RING_PFD * gridDim.x;
+        if (nx < n_items) {
+          const int64_t gn = (p.d_begin >> 3) + (TILED ? item_nat(nx, p, lz) : nx) * NB;
+          const BlkCoord cn = block_coord(gn * 8 * F, p);
+          const int64_t nb = block_neighbor<0, true>(gn * 8 * F, cn, p) / (8 * F);
+          const char* base = reinterpret_cast<const char*>(src + nb * 96 * B);
+          constexpr int kLines = (int)(Sh::SPIN * sizeof(C) / 128);
+          for (int ln = tid; ln < kLines; ln += Sh::NC)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (size_t)ln * 128));
+        }
+      }
+      if constexpr ((B200WD_RING_EXP & 1) != 0) {
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+#pragma unroll
+          for (int k = 0; k < 12; ++k) acc[v][k] = mk(R(0), R(0));
+      } else {
       if (self_is_src || p.xself) {
         const C* xp = self_is_src ? zt + j * 96 * B + lo * B + r0
                                   : static_cast<const C*>(p.xself) + spinor_base(d, 12, B) + r0;
@@ -604,6 +701,7 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
                                                    U + link_base(xp, 3, nblk), 8);
         }
       }
+      }  // !(B200WD_RING_EXP & 1)
       __syncwarp();
       if (lead) mbar_arrive(&empty[slot]);
       if (++cslot == S) {
@@ -617,7 +715,8 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
     const int slot = cslot;                                                                          \
     mbar_wait(&full[slot], cphase);                                                                  \
     const C* sb = ring + slot * Sh::SLOT;                                                            \
-    if (HALO && (H) == 0 && item_t == p.T - 1)                                                       \
+    if ((B200WD_RING_EXP & 1) != 0) {                                                                \
+    } else if (HALO && (H) == 0 && item_t == p.T - 1)                                                     \
       hop_lam_halo<R, V, true, true>(acc, sb + (j * 8 + lo) * B + r0, NB * 8 * B, sb + Sh::SPIN + lofs, 8); \
     else if (HALO && (H) == 1 && item_t == 0)                                                        \
       hop_chi_halo<R, V, true>(acc, sb + (j * 8 + lo) * B + r0, NB * 8 * B);                         \
@@ -642,8 +741,10 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
     }                                                                                                \
   }
     bool released = false;
-    B200WD_CONSUME(0)
-    B200WD_CONSUME(1)
+    if (!(B200WD_RING_EXP & 4)) {
+      B200WD_CONSUME(0)
+      B200WD_CONSUME(1)
+    }
     B200WD_CONSUME(2)
     B200WD_CONSUME(3)
     B200WD_CONSUME(4)
@@ -703,7 +804,7 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
         for (int v = 0; v < V; ++v) res[v] = acc[v][k];
         VecIO<R, V>::st(out + k * KST, res);
       }
-    } else {
+    } else if (!(B200WD_RING_EXP & 16)) {
 #pragma unroll
       for (int k = 0; k < 12; ++k) {
         C res[V];
