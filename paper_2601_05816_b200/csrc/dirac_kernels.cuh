@@ -1239,6 +1239,7 @@ __global__ void __launch_bounds__(256) halo_pack_kernel(const HopParams p, void*
 }  // namespace b200wd
 #include "tstream.cuh"
 #include "ring2.cuh"
+#include "march.cuh"
 namespace b200wd {
 
 static bool bulk_enabled() {
@@ -1253,6 +1254,7 @@ static bool bulk_enabled() {
 template <typename R, int V, int B>
 static void launch_hop_b(const HopParams& p, cudaStream_t st) {
   if constexpr (B >= 4) {
+    if (bulk_enabled() && try_launch_march<R, V, B>(p, st)) return;
     if (bulk_enabled() && try_launch_tstream<R, V, B>(p, st)) return;
     if (bulk_enabled() && try_launch_ring2<R, V, B>(p, st)) return;
     if (bulk_enabled() && try_launch_ring<R, V, B>(p, st)) return;
