@@ -28,6 +28,12 @@
 // one SM sub-partition), so the CTA carries a whole producer warpgroup and
 // moves its registers to the consumers with setmaxnreg.
 //
+// An item is LY y-adjacent segments (LY = 1, 2 or 4), sized so that a CTA has
+// 192 or 256 consumer threads.  One CTA per SM always: with two resident CTAs
+// per SM the register reallocation corrupted results on B200 (wrong half
+// spinors in a few warps per launch, gone with either one CTA per SM or
+// without setmaxnreg; profiles/r2_march_tuning.txt).
+//
 // Work units are (t-chunk, column) pairs, columns fastest, so the CTAs running
 // at one time march neighbouring columns through the same slices and their x/y
 // neighbour tiles hit L2.
@@ -41,27 +47,45 @@
 
 namespace b200wd {
 
-template <typename R, int V, int B, int NB> struct MarchShape {
+#ifndef B200WD_MARCH_DEBUG
+#define B200WD_MARCH_DEBUG 0
+#endif
+#ifndef B200WD_MARCH_NOREALLOC
+#define B200WD_MARCH_NOREALLOC 0
+#endif
+#ifndef B200WD_MARCH_REG_C
+#define B200WD_MARCH_REG_C 232
+#define B200WD_MARCH_REG_P 40
+#endif
+#ifndef B200WD_MARCH_RACY
+#define B200WD_MARCH_RACY 0  // experiment: idle producer warps exit at once (corrupts registers)
+#endif
+#ifndef B200WD_MARCH_SAFE
+#define B200WD_MARCH_SAFE 0  // 1: hand buffers back only after their loaded values were consumed
+#endif
+
+template <typename R, int V, int B, int NB, int LY> struct MarchShape {
   static constexpr int BT = B / V;                 // threads per site
-  static constexpr int SEG = 8 * NB;               // sites per column segment
-  static constexpr int NC = BT * SEG;              // consumer threads
+  static constexpr int SEG = 8 * NB;               // sites per line segment
+  static constexpr int NC = BT * SEG * LY;         // consumer threads
   static constexpr int NCW = NC / 32;
-  static constexpr bool REALLOC = NC % 128 == 0;   // whole consumer warpgroups: setmaxnreg
+  static constexpr bool REALLOC = NC == 256 && !B200WD_MARCH_NOREALLOC;       // 8 consumer warps + producer: setmaxnreg (9 warps cap at 168)
   static constexpr int NP = REALLOC ? 128 : 32;    // producer threads (one issues)
   static constexpr int NT = NC + NP;
-  static constexpr int MINB = NC <= 128 ? 2 : 1;
   // registers after reallocation (per SM sub-partition: 16384 >= 32 * sum over its warps)
-  static constexpr int REG_C = MINB == 2 ? 208 : 232;
-  static constexpr int REG_P = 40;
-  static constexpr int SPIN = NB * 96 * B;         // spinor complex per tile
-  static constexpr int LNK = NB * 72;              // link complex per tile, one direction
+  static constexpr int REG_C = B200WD_MARCH_REG_C;
+  static constexpr int REG_P = B200WD_MARCH_REG_P;
+  static constexpr int LSP = NB * 96 * B;          // spinor complex per line segment
+  static constexpr int LLK = NB * 72;              // link complex per line segment, one direction
+  static constexpr int SPIN = LY * LSP;            // spinor complex per tile
+  static constexpr int LNK = LY * LLK;             // link complex per tile, one direction
   static constexpr int SLOT = SPIN + LNK;          // neighbour tile + its link plane
   static constexpr int LST = 2;                    // stages of the own link planes (U_0, U_3)
   static constexpr int SLOT_BYTES = SLOT * (int)sizeof(cx<R>);
   static constexpr size_t smem(int S) {
-    return ((size_t)SPIN + (size_t)S * SLOT + (size_t)LST * 2 * LNK) * sizeof(cx<R>) + 8 * (2 * S + 2 * LST + 2);
+    return ((size_t)SPIN + (size_t)S * SLOT + (size_t)LST * 2 * LNK) * sizeof(cx<R>) + 8 * (2 * S + 2 * LST + 3);
   }
-  static constexpr bool valid = (B % V == 0) && (NC % 32 == 0) && NC >= 64 && NC <= 256 &&
+  static constexpr bool valid = (B % V == 0) && (NC % 32 == 0) && NC >= 128 && NC <= 256 &&
                                 smem(2) <= 227 * 1024;
 };
 
@@ -119,17 +143,49 @@ template <int N> __device__ __forceinline__ void reg_inc() {
 template <int N> __device__ __forceinline__ void reg_dec() {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
 }
-#ifndef B200WD_MARCH_SKEW_NS
-#define B200WD_MARCH_SKEW_NS 0
-#endif
+
+// Work decomposition.  Columns [0, n1) are marched over the whole slice range
+// by one unit each (n1 is a multiple of the grid: whole rounds in which every
+// CTA carries one column through the same slices); the remaining ncol - n1
+// columns are cut into nch2 t chunks each so that they balance over the grid.
+// Units are ordered (chunk, column): the CTAs running at one time march
+// neighbouring columns through the same slices.
+struct MarchGrid {
+  int32_t lz, ny;   // segments per z line, lines in y
+  int64_t ncol;     // X * ny * lz
+  int32_t ta, nT;   // destination slices [ta, ta + nT)
+  int64_t n1;       // columns marched whole
+  int32_t nch2;     // t chunks of the other columns
+  int64_t n_units;  // n1 + (ncol - n1) * nch2
+};
+__device__ __forceinline__ TsUnit march_decode(int64_t u, const MarchGrid& g) {
+  TsUnit w;
+  uint32_t c;
+  if (u < g.n1) {
+    c = (uint32_t)u;
+    w.t0 = g.ta;
+    w.t1 = g.ta + g.nT;
+  } else {
+    const int64_t v = u - g.n1, r = g.ncol - g.n1;
+    const int64_t chunk = v / r;
+    c = (uint32_t)(g.n1 + (v - chunk * r));
+    w.t0 = g.ta + (int)((chunk * g.nT) / g.nch2);
+    w.t1 = g.ta + (int)(((chunk + 1) * g.nT) / g.nch2);
+  }
+  w.zi = (int)(c % (uint32_t)g.lz);
+  c /= (uint32_t)g.lz;
+  w.y = (int)(c % (uint32_t)g.ny);
+  w.x = (int)(c / (uint32_t)g.ny);
+  return w;
+}
 
 // ZG: segments are not whole z lines; the z hops at the segment edges read
 // global memory through generic pointers.
-template <typename R, int V, int B, int NB, bool ZG>
-__global__ void __launch_bounds__(MarchShape<R, V, B, NB>::NT, MarchShape<R, V, B, NB>::MINB)
-    hop_march_kernel(const HopParams p, const TsGrid g, int S) {
+template <typename R, int V, int B, int NB, int LY, bool ZG>
+__global__ void __launch_bounds__(MarchShape<R, V, B, NB, LY>::NT, 1)
+    hop_march_kernel(const HopParams p, const MarchGrid g, int S) {
   using C = cx<R>;
-  using Sh = MarchShape<R, V, B, NB>;
+  using Sh = MarchShape<R, V, B, NB, LY>;
   constexpr int KST = 8 * B;
   constexpr int SEG = Sh::SEG;
   if (hop_stopped(p)) return;
@@ -143,6 +199,7 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB>::NT, MarchShape<R, V, 
   uint64_t* lempty = lfull + Sh::LST;
   uint64_t* own_full = lempty + Sh::LST;  // every warp stored its part of psi(s)
   uint64_t* own_free = own_full + 1;      // every warp is done with the z hops of the step
+  uint64_t* regs_ok = own_free + 1;       // every consumer warp completed setmaxnreg.inc
 
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -156,6 +213,7 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB>::NT, MarchShape<R, V, 
     }
     mbar_init(own_full, Sh::NCW);
     mbar_init(own_free, Sh::NCW);
+    mbar_init(regs_ok, Sh::NCW);
     fence_barrier_init();
   }
   __syncthreads();
@@ -167,17 +225,41 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB>::NT, MarchShape<R, V, 
   if (tid >= Sh::NC) {
     // ---------------- producer warpgroup: one lane issues every copy ----------------
     if constexpr (Sh::REALLOC) reg_dec<Sh::REG_P>();
-    if (tid != Sh::NC) return;
+    // The idle warps of the producer warpgroup leave only after every consumer warp
+    // holds its reallocated registers (regs_ok): when they exited right after
+    // setmaxnreg.dec, racing the consumers' setmaxnreg.inc, consumer registers were
+    // corrupted at random (a few wrong half spinors per launch on B200; tools/
+    // stress_march.py), and keeping them resident for the whole kernel cost 18%.
+    if (tid >= Sh::NC + 32) {
+      if constexpr (Sh::REALLOC && !B200WD_MARCH_RACY) mbar_wait(regs_ok, 0);
+      return;
+    }
+    if (tid != Sh::NC) return;  // idle lanes of the issuing warp: lanes leaving frees nothing
+    {
     const C* src = static_cast<const C*>(p.src);
     const C* U = static_cast<const C*>(p.U);
     int pslot = 0, pfirst = 1, ls = 0, lfirst = 1;
     uint32_t pphase = 0, lphase = 0;
-    auto tile = [&](int64_t bn, int64_t bl, int mu) {
+    const bool whole = g.lz == 1;
+    // LY lines y0 .. y0+LY-1 (mod Y) of segment zi at (t, x): NB blocks of `per` complex
+    // each per line, from `base`; one copy when the lines are contiguous in memory
+    auto lines = [&](C* dst, const C* base, int per, int t, int x, int y0, int zi, uint64_t* bar) {
+      if (LY == 1 || (whole && y0 >= 0 && y0 + LY <= p.Y)) {
+        bulk_g2s(dst, base + ts_blk(t, x, wrapi(y0, p.Y), zi, p, NB) * per, (uint32_t)(LY * NB * per * sizeof(C)), bar);
+      } else {
+#pragma unroll
+        for (int l = 0; l < LY; ++l)
+          bulk_g2s(dst + l * NB * per, base + ts_blk(t, x, wrapi(y0 + l, p.Y), zi, p, NB) * per,
+                   (uint32_t)(NB * per * sizeof(C)), bar);
+      }
+    };
+    // neighbour tile: spinor lines (xs, ys..) and one link direction of lines (xl, yl..)
+    auto tile = [&](int s, int xs, int ys, int xl, int yl, int zi, int mu) {
       if (!pfirst) mbar_wait(&empty[pslot], pphase ^ 1u);
       C* slot = ring + pslot * Sh::SLOT;
       mbar_expect_tx(&full[pslot], (uint32_t)(Sh::SLOT * sizeof(C)));
-      bulk_g2s(slot, src + bn * SB, (uint32_t)(Sh::SPIN * sizeof(C)), &full[pslot]);
-      bulk_g2s(slot + Sh::SPIN, U + (mu * nblk + bl) * 72, (uint32_t)(Sh::LNK * sizeof(C)), &full[pslot]);
+      lines(slot, src, SB, s, xs, ys, zi, &full[pslot]);
+      lines(slot + Sh::SPIN, U + mu * nblk * 72, 72, s, xl, yl, zi, &full[pslot]);
       if (++pslot == S) {
         pslot = 0;
         pphase ^= 1u;
@@ -185,48 +267,53 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB>::NT, MarchShape<R, V, 
       }
     };
     for (int64_t u = blockIdx.x; u < g.n_units; u += gridDim.x) {
-      const TsUnit w = ts_decode(u, g);
+      const TsUnit w = march_decode(u, g);
+      const int y0 = w.y * LY;  // first line of the item
       for (int s = w.t0; s < w.t1; ++s) {
-        const int64_t b0 = ts_blk(s, w.x, w.y, w.zi, p, NB);
         {  // U_0 and U_3 of the own blocks
           if (!lfirst) mbar_wait(&lempty[ls], lphase ^ 1u);
           C* d = lks + ls * 2 * Sh::LNK;
           mbar_expect_tx(&lfull[ls], (uint32_t)(2 * Sh::LNK * sizeof(C)));
-          bulk_g2s(d, U + (0 * nblk + b0) * 72, (uint32_t)(Sh::LNK * sizeof(C)), &lfull[ls]);
-          bulk_g2s(d + Sh::LNK, U + (3 * nblk + b0) * 72, (uint32_t)(Sh::LNK * sizeof(C)), &lfull[ls]);
+          lines(d, U + 0 * nblk * 72, 72, s, w.x, y0, w.zi, &lfull[ls]);
+          lines(d + Sh::LNK, U + 3 * nblk * 72, 72, s, w.x, y0, w.zi, &lfull[ls]);
           if (++ls == Sh::LST) {
             ls = 0;
             lphase ^= 1u;
             lfirst = 0;
           }
         }
-        const int64_t bxp = ts_blk(s, wrapi(w.x + 1, p.X), w.y, w.zi, p, NB);
-        const int64_t bxm = ts_blk(s, wrapi(w.x - 1, p.X), w.y, w.zi, p, NB);
-        const int64_t byp = ts_blk(s, w.x, wrapi(w.y + 1, p.Y), w.zi, p, NB);
-        const int64_t bym = ts_blk(s, w.x, wrapi(w.y - 1, p.Y), w.zi, p, NB);
-        tile(bxp, b0, 1);
-        tile(bxm, bxm, 1);
-        tile(byp, b0, 2);
-        tile(bym, bym, 2);
+        const int xp = wrapi(w.x + 1, p.X), xm = wrapi(w.x - 1, p.X);
+        tile(s, xp, y0, w.x, y0, w.zi, 1);          // x+: U_1 of the own lines
+        tile(s, xm, y0, xm, y0, w.zi, 1);           // x-: U_1 of the neighbour lines
+        tile(s, w.x, y0 + 1, w.x, y0, w.zi, 2);     // y+: lines y0+1 .., U_2 of the own lines
+        tile(s, w.x, y0 - 1, w.x, y0 - 1, w.zi, 2); // y-: lines y0-1 .., their U_2
         if (s == w.t1 - 1 && u + gridDim.x < g.n_units) {
-          // warm L2 with the two own tiles the next unit's prologue loads
-          const TsUnit wn = ts_decode(u + gridDim.x, g);
-          bulk_prefetch_l2(src + ts_blk(wrapi(wn.t0 - 1, p.T), wn.x, wn.y, wn.zi, p, NB) * SB,
-                           (uint32_t)(Sh::SPIN * sizeof(C)));
-          bulk_prefetch_l2(src + ts_blk(wn.t0, wn.x, wn.y, wn.zi, p, NB) * SB, (uint32_t)(Sh::SPIN * sizeof(C)));
-          bulk_prefetch_l2(U + ts_blk(wrapi(wn.t0 - 1, p.T), wn.x, wn.y, wn.zi, p, NB) * 72,
-                           (uint32_t)(Sh::LNK * sizeof(C)));
+          // warm L2 with what the next unit's prologue loads: two own tiles and U_0(t0-1)
+          const TsUnit wn = march_decode(u + gridDim.x, g);
+          const int tm = wrapi(wn.t0 - 1, p.T);
+#pragma unroll
+          for (int l = 0; l < LY; ++l) {
+            bulk_prefetch_l2(src + ts_blk(tm, wn.x, wn.y * LY + l, wn.zi, p, NB) * SB, (uint32_t)(Sh::LSP * sizeof(C)));
+            bulk_prefetch_l2(src + ts_blk(wn.t0, wn.x, wn.y * LY + l, wn.zi, p, NB) * SB,
+                             (uint32_t)(Sh::LSP * sizeof(C)));
+            bulk_prefetch_l2(U + ts_blk(tm, wn.x, wn.y * LY + l, wn.zi, p, NB) * 72, (uint32_t)(Sh::LLK * sizeof(C)));
+          }
         }
       }
+    }
     }
     return;
   }
 
   // ---------------- consumers ----------------
-  if constexpr (Sh::REALLOC) reg_inc<Sh::REG_C>();
+  if constexpr (Sh::REALLOC) {
+    reg_inc<Sh::REG_C>();
+    if ((tid & 31) == 0) mbar_arrive(regs_ok);
+  }
   const int r0 = (tid % Sh::BT) * V;
-  const int ys = tid / Sh::BT;         // site in the segment
-  const int j = ys >> 3, lo = ys & 7;  // block, site in block
+  const int ys = tid / Sh::BT;                 // site in the item
+  const int ln = ys / SEG, zs = ys % SEG;      // line of the item, z offset in its segment
+  const int j = ln * NB + (zs >> 3), lo = zs & 7;  // block of the tile, site in block
   const int so = (j * 96 + lo) * B + r0;   // own spinor (k = 0) in a tile
   const int lofs = j * 72 + lo;            // own link (e = 0) in a plane
   const bool lead = (tid & 31) == 0;
@@ -241,16 +328,12 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB>::NT, MarchShape<R, V, 
   int cslot = 0, ls = 0;
   uint32_t cphase = 0, lphase = 0, ophase = 0;
   if (lead) mbar_arrive(own_free);  // phase 0: the own tile starts out free
-  // The consumer warps are never synchronised as a group (the own tile is
-  // handed over through mbarriers waited on long after their completion), so
-  // a one-time skew of every other warp persists: while one warp of an SM
-  // sub-partition loads from shared memory the other one computes.
-  if (B200WD_MARCH_SKEW_NS > 0 && ((tid >> 5) & 1)) __nanosleep(B200WD_MARCH_SKEW_NS);
 
   for (int64_t u = blockIdx.x; u < g.n_units; u += gridDim.x) {
-    const TsUnit w = ts_decode(u, g);
-    const int z = w.zi * SEG + ys;
-    const int64_t col_blk = ((int64_t)w.x * p.Y + w.y) * (int64_t)(p.Z >> 3) + (int64_t)w.zi * NB + j;
+    const TsUnit w = march_decode(u, g);
+    const int z = w.zi * SEG + zs;
+    const int yl = w.y * LY + ln;  // this thread's line
+    const int64_t col_blk = ((int64_t)w.x * p.Y + yl) * (int64_t)(p.Z >> 3) + (int64_t)w.zi * NB + (zs >> 3);
     // element (k = 0) of this thread's site in slice t
     auto elem = [&](int t) { return ((int64_t)t * slice_blks + col_blk) * SB + lo * B + r0; };
     C nxt[V][12];       // psi(s) at the top of step s, psi(s+1) from its middle on
@@ -285,13 +368,40 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB>::NT, MarchShape<R, V, 
     }
     for (int s = w.t0; s < w.t1; ++s) {
       C acc[V][12];
-      mbar_wait(own_free, ophase);  // every warp is done with the z hops of the previous step (long ago)
+      // own link planes of this step
+      mbar_wait(&lfull[ls], lphase);
+      const C* lk = lks + ls * 2 * Sh::LNK;
+      {
+        // z hops, sender side: this site's half spinors for its two z neighbours --
+        // P-_3 psi(s) for the forward hop of z-1 (multiplied there by U_3(z-1)) and
+        // U_3(z)^H P+_3 psi(s), the finished backward hop of z+1 -- go to the own
+        // tile as components 0-5 and 6-11: 12 stores as for psi itself, but the
+        // receivers read 6 + 6 instead of 12 + 12 components and one link less
+        C um[9];
 #pragma unroll
-      for (int k = 0; k < 12; ++k) {
-        C tmp[V];
+        for (int e = 0; e < 9; ++e) um[e] = lk[Sh::LNK + lofs + e * 8];
+        C hf[V][2][3], hb[V][2][3];
 #pragma unroll
-        for (int v = 0; v < V; ++v) tmp[v] = nxt[v][k];
-        StS<R, V>::st(own + so + k * KST, tmp);
+        for (int v = 0; v < V; ++v) {
+          C h[2][3];
+          project_spin<3, true, 0>(hf[v][0], nxt[v]);
+          project_spin<3, true, 1>(hf[v][1], nxt[v]);
+          project_spin<3, false, 0>(h[0], nxt[v]);
+          project_spin<3, false, 1>(h[1], nxt[v]);
+          matvec2<true>(hb[v], um, h);
+        }
+        mbar_wait(own_free, ophase);  // every warp is done with the z hops of the previous step (long ago)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          C t0[V], t1[V];
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            t0[v] = hf[v][k / 3][k % 3];
+            t1[v] = hb[v][k / 3][k % 3];
+          }
+          StS<R, V>::st(own + so + k * KST, t0);
+          StS<R, V>::st(own + so + (6 + k) * KST, t1);
+        }
       }
       __syncwarp();
       if (lead) mbar_arrive(own_full);
@@ -322,9 +432,6 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB>::NT, MarchShape<R, V, 
         accumulate_spin<0, false, 0>(acc[v], carry[v]);
         accumulate_spin<0, false, 1>(acc[v], carry[v]);
       }
-      // own link planes of this step
-      mbar_wait(&lfull[ls], lphase);
-      const C* lk = lks + ls * 2 * Sh::LNK;
       {  // next carry: U_0(s)^H P+ psi(s)
         C um[9];
 #pragma unroll
@@ -351,46 +458,97 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB>::NT, MarchShape<R, V, 
   {                                                                             \
     mbar_wait(&full[cslot], cphase);                                            \
     const C* sb = ring + cslot * Sh::SLOT;                                      \
+    if (B200WD_MARCH_DEBUG) {                                                   \
+      const int xx = MU == 1 ? wrapi(w.x + (FWD ? 1 : -1), p.X) : w.x;          \
+      const int yy = MU == 2 ? wrapi(yl + (FWD ? 1 : -1), p.Y) : yl;            \
+      const int64_t nblkk = (((int64_t)s * p.X + xx) * p.Y + yy) * (int64_t)(p.Z >> 3) + (int64_t)w.zi * NB + (zs >> 3); \
+      const C* gp = src + nblkk * SB + lo * B + r0;                             \
+      const int64_t lblk = FWD ? (((int64_t)s * p.X + w.x) * p.Y + yl) * (int64_t)(p.Z >> 3) + (int64_t)w.zi * NB + (zs >> 3) : nblkk; \
+      const C* gl = U + (MU * nblk + lblk) * 72 + lo;                           \
+      for (int k = 0; k < 12; ++k) {                                            \
+        const C a = sb[so + k * KST], g2 = gp[k * KST];                         \
+        if (a.x != g2.x || a.y != g2.y)                                         \
+          printf("SPIN cta %d tid %d s %d x %d y %d zi %d mu %d fwd %d k %d slot %d ph %d\n", (int)blockIdx.x, tid, s, w.x, yl, w.zi, MU, (int)FWD, k, cslot, (int)cphase); \
+      }                                                                         \
+      for (int e = 0; e < 9; ++e) {                                             \
+        const C a = sb[Sh::SPIN + lofs + e * 8], g2 = gl[e * 8];                \
+        if (a.x != g2.x || a.y != g2.y)                                         \
+          printf("LINK cta %d tid %d s %d x %d y %d zi %d mu %d fwd %d e %d slot %d ph %d\n", (int)blockIdx.x, tid, s, w.x, yl, w.zi, MU, (int)FWD, e, cslot, (int)cphase); \
+      }                                                                         \
+    }                                                                           \
     HopRegs<R, V> hr;                                                           \
     hop_load<MU, FWD, R, V, KST>(hr, sb + so, sb + Sh::SPIN + lofs);            \
+    if (B200WD_MARCH_SAFE) hop_compute<MU, FWD, R, V>(acc, hr);                 \
     __syncwarp();                                                               \
     if (lead) mbar_arrive(&empty[cslot]);                                       \
     if (++cslot == S) {                                                         \
       cslot = 0;                                                                \
       cphase ^= 1u;                                                             \
     }                                                                           \
-    hop_compute<MU, FWD, R, V>(acc, hr);                                        \
+    if (!B200WD_MARCH_SAFE) hop_compute<MU, FWD, R, V>(acc, hr);                \
   }
       B200WD_MARCH_TILE(1, true)
       B200WD_MARCH_TILE(1, false)
       B200WD_MARCH_TILE(2, true)
       mbar_wait(own_full, ophase);  // the own tile is complete (every warp stored its part at the top of the step)
-      {  // z hops from the own tile, U_3 in the second plane
+      {  // z hops, receiver side (U_3 in the second link plane)
         const C* ua = lk + Sh::LNK;
-        const int zp = ys + 1, zm = ys - 1;
-        if constexpr (!ZG) {
-          const int zpp = zp == SEG ? 0 : zp, zmm = zm < 0 ? SEG - 1 : zm;
-          hop_full<3, true, R, V, true, true>(acc, own + ((zpp >> 3) * 96 + (zpp & 7)) * B + r0, KST, ua + lofs, 8);
-          hop_full<3, false, R, V, true, true>(acc, own + ((zmm >> 3) * 96 + (zmm & 7)) * B + r0, KST,
-                                               ua + (zmm >> 3) * 72 + (zmm & 7), 8);
-        } else {
-          const int64_t line0 = (int64_t)s * p.per_t + ((int64_t)w.x * p.Y + w.y) * p.Z;  // first site of the z line
-          {
-            const C* sp = zp < SEG ? own + ((zp >> 3) * 96 + (zp & 7)) * B + r0
-                                   : src + spinor_base(line0 + wrapi(z + 1, p.Z), 12, B) + r0;
-            hop_full<3, true, R, V, true, true>(acc, sp, KST, ua + lofs, 8);
+        const int zp = zs + 1, zm = zs - 1;
+        auto fwd_in = [&](int zz) {  // U_3(z) applied to the neighbour's P- half spinor
+          const C* hp = own + ((ln * NB + (zz >> 3)) * 96 + (zz & 7)) * B + r0;
+          C um[9];
+#pragma unroll
+          for (int e = 0; e < 9; ++e) um[e] = ua[lofs + e * 8];
+          C hh[V][2][3];
+#pragma unroll
+          for (int k = 0; k < 6; ++k) {
+            C tmp[V];
+            VecIO<R, V>::lds(tmp, hp + k * KST);
+#pragma unroll
+            for (int v = 0; v < V; ++v) hh[v][k / 3][k % 3] = tmp[v];
           }
-          {
-            const C *sp, *up;
-            if (zm >= 0) {
-              sp = own + ((zm >> 3) * 96 + (zm & 7)) * B + r0;
-              up = ua + (zm >> 3) * 72 + (zm & 7);
-            } else {
-              const int64_t xs = line0 + wrapi(z - 1, p.Z);
-              sp = src + spinor_base(xs, 12, B) + r0;
-              up = U + link_base(xs, 3, nblk);
-            }
-            hop_full<3, false, R, V, true, true>(acc, sp, KST, up, 8);
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            C gg[2][3];
+            matvec2<false>(gg, um, hh[v]);
+            accumulate_spin<3, true, 0>(acc[v], gg);
+            accumulate_spin<3, true, 1>(acc[v], gg);
+          }
+        };
+        auto bwd_in = [&](int zz) {  // the neighbour's finished backward hop
+          const C* hp = own + ((ln * NB + (zz >> 3)) * 96 + (zz & 7)) * B + r0 + 6 * KST;
+          C gg[V][2][3];
+#pragma unroll
+          for (int k = 0; k < 6; ++k) {
+            C tmp[V];
+            VecIO<R, V>::lds(tmp, hp + k * KST);
+#pragma unroll
+            for (int v = 0; v < V; ++v) gg[v][k / 3][k % 3] = tmp[v];
+          }
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            accumulate_spin<3, false, 0>(acc[v], gg[v]);
+            accumulate_spin<3, false, 1>(acc[v], gg[v]);
+          }
+        };
+        if constexpr (!ZG) {
+          fwd_in(zp == SEG ? 0 : zp);
+          bwd_in(zm < 0 ? SEG - 1 : zm);
+        } else {
+          // segment edges: the neighbour belongs to another column, whole hop from global memory
+          const int64_t line0 = (int64_t)s * p.per_t + ((int64_t)w.x * p.Y + yl) * p.Z;  // first site of the z line
+          if (zp < SEG) {
+            fwd_in(zp);
+          } else {
+            hop_full<3, true, R, V, false, true>(acc, src + spinor_base(line0 + wrapi(z + 1, p.Z), 12, B) + r0, KST,
+                                                 ua + lofs, 8);
+          }
+          if (zm >= 0) {
+            bwd_in(zm);
+          } else {
+            const int64_t xs = line0 + wrapi(z - 1, p.Z);
+            hop_full<3, false, R, V, false, false>(acc, src + spinor_base(xs, 12, B) + r0, KST,
+                                                   U + link_base(xs, 3, nblk), 8);
           }
         }
       }
@@ -401,11 +559,9 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB>::NT, MarchShape<R, V, 
         C um[9];
 #pragma unroll
         for (int e = 0; e < 9; ++e) um[e] = lk[lofs + e * 8];
-        __syncwarp();
-        if (lead) mbar_arrive(&lempty[ls]);
-        if (++ls == Sh::LST) {
-          ls = 0;
-          lphase ^= 1u;
+        if (!B200WD_MARCH_SAFE) {
+          __syncwarp();
+          if (lead) mbar_arrive(&lempty[ls]);
         }
 #pragma unroll
         for (int v = 0; v < V; ++v) {
@@ -415,6 +571,14 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB>::NT, MarchShape<R, V, 
           matvec2<false>(gg, um, h);
           accumulate_spin<0, true, 0>(acc[v], gg);
           accumulate_spin<0, true, 1>(acc[v], gg);
+        }
+        if (B200WD_MARCH_SAFE) {
+          __syncwarp();
+          if (lead) mbar_arrive(&lempty[ls]);
+        }
+        if (++ls == Sh::LST) {
+          ls = 0;
+          lphase ^= 1u;
         }
       }
       B200WD_MARCH_TILE(2, false)
@@ -434,14 +598,15 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB>::NT, MarchShape<R, V, 
 // ---- host side ----------------------------------------------------------------
 
 struct MarchCfg {
-  int nb = 0, s = 0, nch = 0;
+  int nb = 0, ly = 0, s = 0, nch = 0;
 };
+// B200WD_MARCH_CFG="NB,LY,S,NCH" forces a shape (0: default for that field)
 static MarchCfg march_env() {
-  static MarchCfg c{-1, -1, -1};
+  static MarchCfg c{-1, -1, -1, -1};
   if (c.nb < 0) {
     c = MarchCfg{};
     const char* e = getenv("B200WD_MARCH_CFG");
-    if (e) sscanf(e, "%d,%d,%d", &c.nb, &c.s, &c.nch);
+    if (e) sscanf(e, "%d,%d,%d,%d", &c.nb, &c.ly, &c.s, &c.nch);
   }
   return c;
 }
@@ -455,49 +620,78 @@ static int march_mode() {
   return m;
 }
 
-template <typename R, int V, int B, int NB, bool ZG>
-static bool launch_march_kernel(const HopParams& p, const TsGrid& g0, int S, int nch, cudaStream_t st) {
-  using Sh = MarchShape<R, V, B, NB>;
+template <typename R, int V, int B, int NB, int LY, bool ZG>
+static bool launch_march_kernel(const HopParams& p, const MarchGrid& g0, int S, int nch, cudaStream_t st) {
+  using Sh = MarchShape<R, V, B, NB, LY>;
   const size_t smem = Sh::smem(S);
   LaunchFacts f;
-  if (!launch_facts((const void*)hop_march_kernel<R, V, B, NB, ZG>, Sh::NT, smem, f)) return false;
-  TsGrid g = g0;
-  const int64_t grid_max = (int64_t)f.occ * persistent_sms(f.sm_count);
-  g.nch = nch > 0 ? (nch > g.nT ? g.nT : nch) : ts_choose_nch(g.ncol, g.nT, grid_max, 5);
-  g.n_units = g.ncol * g.nch;
+  if (!launch_facts((const void*)hop_march_kernel<R, V, B, NB, LY, ZG>, Sh::NT, smem, f)) return false;
+  MarchGrid g = g0;
+  // one CTA per SM whatever the occupancy calculator allows (see the header)
+  int64_t grid_max = persistent_sms(f.sm_count);
+  static const int grid_cap = ring_knob("B200WD_MARCH_GRID", 0);  // tuning / debugging: cap the persistent grid
+  if (grid_cap > 0 && grid_cap < grid_max) grid_max = grid_cap;
+  if (nch > 0) {  // forced: every column in nch chunks
+    g.n1 = 0;
+    g.nch2 = nch > g.nT ? g.nT : nch;
+  } else {
+    g.n1 = (g.ncol / grid_max) * grid_max;
+    g.nch2 = g.ncol > g.n1 ? ts_choose_nch(g.ncol - g.n1, g.nT, grid_max, 5) : 1;
+  }
+  g.n_units = g.n1 + (g.ncol - g.n1) * g.nch2;
   const int64_t grid = grid_max < g.n_units ? grid_max : g.n_units;
-  hop_march_kernel<R, V, B, NB, ZG><<<(unsigned)grid, Sh::NT, smem, st>>>(p, g, S);
+  hop_march_kernel<R, V, B, NB, LY, ZG><<<(unsigned)grid, Sh::NT, smem, st>>>(p, g, S);
   return true;
 }
 
-template <typename R, int V, int B, int NB>
-static bool launch_march_nb(const HopParams& p, int S, int nch, cudaStream_t st) {
-  using Sh = MarchShape<R, V, B, NB>;
+template <typename R, int V, int B, int NB, int LY>
+static bool launch_march_shape(const HopParams& p, int S, int nch, cudaStream_t st) {
+  using Sh = MarchShape<R, V, B, NB, LY>;
   if constexpr (!Sh::valid) {
     return false;
   } else {
-    if (p.Z % Sh::SEG) return false;
-    TsGrid g{};
+    if (p.Z % Sh::SEG || p.Y % LY) return false;
+    MarchGrid g{};
     g.lz = p.Z / Sh::SEG;
-    g.ny = p.Y;
+    g.ny = p.Y / LY;
     g.ncol = (int64_t)p.X * g.ny * g.lz;
     g.ta = (int32_t)(p.d_begin / p.per_t);
     g.nT = (int32_t)((p.d_end - p.d_begin) / p.per_t);
-    const size_t budget = (Sh::MINB == 2 ? 113 : 227) * 1024;
+    // more than half the shared memory: a second CTA can never become resident
+    const size_t floor_bytes = 116 * 1024;
     if (S <= 0) S = 8;
     if (S > 8) S = 8;
-    while (S > 2 && Sh::smem(S) > budget) --S;
+    while (S > 2 && Sh::smem(S) > 227 * 1024) --S;
     if (Sh::smem(S) > 227 * 1024) return false;
-    if (g.lz == 1) return launch_march_kernel<R, V, B, NB, false>(p, g, S, nch, st);
-    return launch_march_kernel<R, V, B, NB, true>(p, g, S, nch, st);
+    size_t smem = Sh::smem(S);
+    (void)smem;
+    if (Sh::smem(S) < floor_bytes) return false;  // small tiles: the ring kernels serve those shapes
+    if (g.lz == 1) return launch_march_kernel<R, V, B, NB, LY, false>(p, g, S, nch, st);
+    return launch_march_kernel<R, V, B, NB, LY, true>(p, g, S, nch, st);
   }
 }
 
-// Where the march is the default: (NB, S) per (dtype, b); nb = 0: not used.
+// Default shape: whole z lines when a line fits 256 consumer threads, else the
+// largest segment that does; then as many y lines as keep the item at or below
+// 256 threads.
 template <typename R, int V, int B>
-static MarchCfg march_table(int Z) {
-  (void)Z;
-  return MarchCfg{};
+static MarchCfg march_default_shape(const HopParams& p) {
+  MarchCfg c{};
+  constexpr int BT = B / V;
+  for (int nb : {4, 2, 1})
+    if (c.nb == 0 && p.Z % (8 * nb) == 0 && BT * 8 * nb <= 256) c.nb = nb;
+  if (c.nb == 0) return c;
+  for (int ly : {4, 2, 1})
+    if (c.ly == 0 && p.Y % ly == 0 && BT * 8 * c.nb * ly <= 256) c.ly = ly;
+  return c;
+}
+
+// Where the march is the default (measured against the ring kernels,
+// profiles/r2_march_tuning.txt); B200WD_MARCH=1 forces it wherever a shape exists.
+template <typename R, int V, int B>
+static bool march_table(const HopParams& p) {
+  (void)p;
+  return false;
 }
 
 // Full-lattice fields, no halos, no clover, slice-aligned destination range.
@@ -508,21 +702,25 @@ static bool try_launch_march(const HopParams& p, cudaStream_t st) {
   if (p.dst_parity >= 0 || p.lam_halo != nullptr || p.beta == 0.0 || p.clov_mode != 0 || p.jump_by) return false;
   if (p.Z % 8 != 0) return false;
   if (p.d_begin % p.per_t || p.d_end % p.per_t || p.d_end <= p.d_begin) return false;
-  MarchCfg c = march_table<R, V, B>(p.Z);
   const MarchCfg e = march_env();
-  if (mode != 1 && e.nb <= 0 && c.nb <= 0) return false;
-  if (e.nb > 0) c.nb = e.nb;
+  if (mode != 1 && e.nb <= 0 && !march_table<R, V, B>(p)) return false;
+  MarchCfg c = march_default_shape<R, V, B>(p);
+  if (e.nb > 0) {
+    c.nb = e.nb;
+    c.ly = e.ly > 0 ? e.ly : 1;
+  }
   if (e.s > 0) c.s = e.s;
   if (e.nch > 0) c.nch = e.nch;
-  if (c.nb <= 0) {  // the largest segment dividing the z line that fits 256 consumer threads
-    for (int nb : {4, 2, 1})
-      if (c.nb <= 0 && p.Z % (8 * nb) == 0 && (B / V) * 8 * nb <= 256) c.nb = nb;
-  }
-#define B200WD_MARCH_TRY(NB_) \
-  if (c.nb == NB_ && launch_march_nb<R, V, B, NB_>(p, c.s, c.nch, st)) return true;
-  B200WD_MARCH_TRY(1)
-  B200WD_MARCH_TRY(2)
-  B200WD_MARCH_TRY(4)
+#define B200WD_MARCH_TRY(NB_, LY_) \
+  if (c.nb == NB_ && c.ly == LY_ && launch_march_shape<R, V, B, NB_, LY_>(p, c.s, c.nch, st)) return true;
+  B200WD_MARCH_TRY(1, 1)
+  B200WD_MARCH_TRY(2, 1)
+  B200WD_MARCH_TRY(4, 1)
+  B200WD_MARCH_TRY(1, 2)
+  B200WD_MARCH_TRY(2, 2)
+  B200WD_MARCH_TRY(4, 2)
+  B200WD_MARCH_TRY(1, 4)
+  B200WD_MARCH_TRY(2, 4)
 #undef B200WD_MARCH_TRY
   return false;
 }
