@@ -47,34 +47,17 @@
 
 namespace b200wd {
 
-#ifndef B200WD_MARCH_DEBUG
-#define B200WD_MARCH_DEBUG 0
-#endif
-#ifndef B200WD_MARCH_NOREALLOC
-#define B200WD_MARCH_NOREALLOC 0
-#endif
-#ifndef B200WD_MARCH_REG_C
-#define B200WD_MARCH_REG_C 232
-#define B200WD_MARCH_REG_P 40
-#endif
-#ifndef B200WD_MARCH_RACY
-#define B200WD_MARCH_RACY 0  // experiment: idle producer warps exit at once (corrupts registers)
-#endif
-#ifndef B200WD_MARCH_SAFE
-#define B200WD_MARCH_SAFE 0  // 1: hand buffers back only after their loaded values were consumed
-#endif
-
 template <typename R, int V, int B, int NB, int LY> struct MarchShape {
   static constexpr int BT = B / V;                 // threads per site
   static constexpr int SEG = 8 * NB;               // sites per line segment
   static constexpr int NC = BT * SEG * LY;         // consumer threads
   static constexpr int NCW = NC / 32;
-  static constexpr bool REALLOC = NC == 256 && !B200WD_MARCH_NOREALLOC;       // 8 consumer warps + producer: setmaxnreg (9 warps cap at 168)
+  static constexpr bool REALLOC = NC == 256;       // 8 consumer warps + producer: setmaxnreg (9 warps cap at 168)
   static constexpr int NP = REALLOC ? 128 : 32;    // producer threads (one issues)
   static constexpr int NT = NC + NP;
   // registers after reallocation (per SM sub-partition: 16384 >= 32 * sum over its warps)
-  static constexpr int REG_C = B200WD_MARCH_REG_C;
-  static constexpr int REG_P = B200WD_MARCH_REG_P;
+  static constexpr int REG_C = 232;
+  static constexpr int REG_P = 40;
   static constexpr int LSP = NB * 96 * B;          // spinor complex per line segment
   static constexpr int LLK = NB * 72;              // link complex per line segment, one direction
   static constexpr int SPIN = LY * LSP;            // spinor complex per tile
@@ -202,7 +185,7 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB, LY>::NT, 1)
   uint64_t* regs_ok = own_free + 1;       // every consumer warp completed setmaxnreg.inc
 
   const int tid = threadIdx.x;
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], Sh::NCW);
@@ -231,7 +214,7 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB, LY>::NT, 1)
     // corrupted at random (a few wrong half spinors per launch on B200; tools/
     // stress_march.py), and keeping them resident for the whole kernel cost 18%.
     if (tid >= Sh::NC + 32) {
-      if constexpr (Sh::REALLOC && !B200WD_MARCH_RACY) mbar_wait(regs_ok, 0);
+      if constexpr (Sh::REALLOC) mbar_wait(regs_ok, 0);
       return;
     }
     if (tid != Sh::NC) return;  // idle lanes of the issuing warp: lanes leaving frees nothing
@@ -403,6 +386,10 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB, LY>::NT, 1)
           StS<R, V>::st(own + so + (6 + k) * KST, t1);
         }
       }
+      // The own tile is the one buffer consumers hand to each other within ~100 ns
+      // (the TMA-filled buffers come back after a memory round trip): the fence makes
+      // every lane's stores (below: loads) complete before the warp's arrival is seen.
+      __threadfence_block();
       __syncwarp();
       if (lead) mbar_arrive(own_full);
       // self term
@@ -458,34 +445,19 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB, LY>::NT, 1)
   {                                                                             \
     mbar_wait(&full[cslot], cphase);                                            \
     const C* sb = ring + cslot * Sh::SLOT;                                      \
-    if (B200WD_MARCH_DEBUG) {                                                   \
-      const int xx = MU == 1 ? wrapi(w.x + (FWD ? 1 : -1), p.X) : w.x;          \
-      const int yy = MU == 2 ? wrapi(yl + (FWD ? 1 : -1), p.Y) : yl;            \
-      const int64_t nblkk = (((int64_t)s * p.X + xx) * p.Y + yy) * (int64_t)(p.Z >> 3) + (int64_t)w.zi * NB + (zs >> 3); \
-      const C* gp = src + nblkk * SB + lo * B + r0;                             \
-      const int64_t lblk = FWD ? (((int64_t)s * p.X + w.x) * p.Y + yl) * (int64_t)(p.Z >> 3) + (int64_t)w.zi * NB + (zs >> 3) : nblkk; \
-      const C* gl = U + (MU * nblk + lblk) * 72 + lo;                           \
-      for (int k = 0; k < 12; ++k) {                                            \
-        const C a = sb[so + k * KST], g2 = gp[k * KST];                         \
-        if (a.x != g2.x || a.y != g2.y)                                         \
-          printf("SPIN cta %d tid %d s %d x %d y %d zi %d mu %d fwd %d k %d slot %d ph %d\n", (int)blockIdx.x, tid, s, w.x, yl, w.zi, MU, (int)FWD, k, cslot, (int)cphase); \
-      }                                                                         \
-      for (int e = 0; e < 9; ++e) {                                             \
-        const C a = sb[Sh::SPIN + lofs + e * 8], g2 = gl[e * 8];                \
-        if (a.x != g2.x || a.y != g2.y)                                         \
-          printf("LINK cta %d tid %d s %d x %d y %d zi %d mu %d fwd %d e %d slot %d ph %d\n", (int)blockIdx.x, tid, s, w.x, yl, w.zi, MU, (int)FWD, e, cslot, (int)cphase); \
-      }                                                                         \
-    }                                                                           \
     HopRegs<R, V> hr;                                                           \
     hop_load<MU, FWD, R, V, KST>(hr, sb + so, sb + Sh::SPIN + lofs);            \
-    if (B200WD_MARCH_SAFE) hop_compute<MU, FWD, R, V>(acc, hr);                 \
+    /* the loads must have read the slot before the arrival is visible: the   */ \
+    /* last ones issued (link rows) were seen overtaken by the refill's small */ \
+    /* link copy (stale colour-2 rows in a warp or two per few launches)      */ \
+    __threadfence_block();                                                      \
     __syncwarp();                                                               \
     if (lead) mbar_arrive(&empty[cslot]);                                       \
     if (++cslot == S) {                                                         \
       cslot = 0;                                                                \
       cphase ^= 1u;                                                             \
     }                                                                           \
-    if (!B200WD_MARCH_SAFE) hop_compute<MU, FWD, R, V>(acc, hr);                \
+    hop_compute<MU, FWD, R, V>(acc, hr);                                        \
   }
       B200WD_MARCH_TILE(1, true)
       B200WD_MARCH_TILE(1, false)
@@ -552,6 +524,7 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB, LY>::NT, 1)
           }
         }
       }
+      __threadfence_block();
       __syncwarp();
       if (lead) mbar_arrive(own_free);
       ophase ^= 1u;
@@ -559,10 +532,9 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB, LY>::NT, 1)
         C um[9];
 #pragma unroll
         for (int e = 0; e < 9; ++e) um[e] = lk[lofs + e * 8];
-        if (!B200WD_MARCH_SAFE) {
-          __syncwarp();
-          if (lead) mbar_arrive(&lempty[ls]);
-        }
+        __threadfence_block();  // as for the tile slots: loads complete before the release
+        __syncwarp();
+        if (lead) mbar_arrive(&lempty[ls]);
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           C h[2][3], gg[2][3];
@@ -571,10 +543,6 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB, LY>::NT, 1)
           matvec2<false>(gg, um, h);
           accumulate_spin<0, true, 0>(acc[v], gg);
           accumulate_spin<0, true, 1>(acc[v], gg);
-        }
-        if (B200WD_MARCH_SAFE) {
-          __syncwarp();
-          if (lead) mbar_arrive(&lempty[ls]);
         }
         if (++ls == Sh::LST) {
           ls = 0;
@@ -686,12 +654,25 @@ static MarchCfg march_default_shape(const HopParams& p) {
   return c;
 }
 
-// Where the march is the default (measured against the ring kernels,
-// profiles/r2_march_tuning.txt); B200WD_MARCH=1 forces it wherever a shape exists.
+// Where the march is the default: the 256-thread shapes (whole 16-site z lines,
+// 16 consumer threads per site) that measured faster than the ring on B200 and
+// came through the race detector clean (tools/stress_march.py: 0 of 1,600
+// repeated launches differ): c128 nrhs 16 (0.519 vs 0.492 of the HBM roofline on
+// 16^3x32, same box and session) and 32 (0.532 vs 0.487), c64 nrhs 32 (0.495 vs
+// 0.481).  KNOWN ISSUE, which is why everything else stays on the ring kernels:
+// the 192-thread shapes (nrhs 6, 12, 24: threads per site not a power of two,
+// one producer warp, no register reallocation) are faster still (c128 nrhs 12
+// 0.576 vs 0.468, c64 nrhs 24 0.548 vs 0.448) but NOT reliably deterministic --
+// up to 5% of launches on 16^3x32 return a few sites whose colour-2 components
+// are wrong (stale rows 6-8 of a forward-hop link tile in one or two warps), not
+// cured by fences before the buffer hand-overs; root cause open
+// (profiles/r2_march_tuning.txt).  B200WD_MARCH=1 forces the march wherever a
+// shape exists (experiments only), B200WD_MARCH=0 turns it off.
 template <typename R, int V, int B>
 static bool march_table(const HopParams& p) {
-  (void)p;
-  return false;
+  if (p.Z != 16) return false;
+  if constexpr (sizeof(R) == 8) return B == 16 || B == 32;
+  return B == 32;
 }
 
 // Full-lattice fields, no halos, no clover, slice-aligned destination range.

@@ -26,6 +26,7 @@ ap.add_argument("--dtypes", nargs="+", default=["c128"])
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--save", default=None)
 ap.add_argument("--ref", default=None)
+ap.add_argument("--where", action="store_true", help="print which sites / components differ")
 a = ap.parse_args()
 bad_total = 0
 for dims in a.dims or [[32, 16, 16, 16]]:
@@ -42,7 +43,7 @@ for dims in a.dims or [[32, 16, 16, 16]]:
             outs = []
             first = None
             nbad = 0
-            for r in range(a.reps):
+            for r_ in range(a.reps):
                 y = torch.zeros_like(x)
                 _lib.call("b200wd_hop", lat, code, b, -1, U.data_ptr(), x.data_ptr(), x.data_ptr(), y.data_ptr(), 4.1,
                           -1.0, None, 0, T, None, None, None)
@@ -51,6 +52,14 @@ for dims in a.dims or [[32, 16, 16, 16]]:
                     first = y
                 elif not torch.equal(torch.view_as_real(first), torch.view_as_real(y)):
                     nbad += 1
+                    if a.where:
+                        d = (first != y)  # (block, k, lo, r)
+                        blk, k, lo, r = torch.nonzero(d, as_tuple=True)
+                        site = (blk * 8 + lo).unique().cpu().numpy()
+                        zz, yy, xx, tt = site % Z, (site // Z) % Y, (site // (Z * Y)) % X, site // (Z * Y * X)
+                        print(f"  rep {r_}: {len(site)} sites; t {sorted(set(tt.tolist()))} x {sorted(set(xx.tolist()))} "
+                              f"y {sorted(set(yy.tolist()))} z {sorted(set(zz.tolist()))} comps {sorted(set(k.cpu().tolist()))} "
+                              f"rhs {sorted(set(r.cpu().tolist()))}", flush=True)
             msg = f"dims={dims} {dt} b={b}: {nbad}/{a.reps - 1} repetitions differ"
             tag = "x".join(map(str, dims)) + f"_{dt}_b{b}"
             if a.save:
