@@ -51,7 +51,7 @@ M0 = 0.1
 METRIC = "D_W apply site*rhs/s (16^3x32, nrhs=16, c128)"
 
 
-PROFILE = ROOT / "profiles" / "r2_ncu_ring_c128_b16_cfg2_final.json"
+PROFILE = ROOT / "profiles" / "r2_ncu_march_c128_b16_cfg2.json"
 
 
 def profile_traffic():
@@ -690,7 +690,7 @@ def main(argv=None):
         "roofline": {"bound": "hbm", "achieved": head["hbm_gbs"], "peak": hbm_peak, "unit": "GB/s",
                      "frac": head["frac"], "traffic": profile_traffic(), "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": head["bytes_per_launch"],
-                     "kernel": "hop_ring_kernel<double,1,16> (libb200wd.so, b200wd_dirac_apply)"},
+                     "kernel": "hop_march_kernel<double,1,16,2,1> (libb200wd.so, b200wd_dirac_apply)"},
         "e2e": e2e, "gpu_launches": args.steps, "clocks": clk,
         "e2e_variants": {"pinned_links_every_call": gpu_e2e(args, torch, P),
                          "pageable_links_every_call": gpu_e2e(args, torch, P, pinned=False)},
