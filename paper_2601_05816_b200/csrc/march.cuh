@@ -47,6 +47,10 @@
 
 namespace b200wd {
 
+#ifndef B200WD_MARCH_RACY
+#define B200WD_MARCH_RACY 0  // experiments: 1 idle producer warps exit at once (corrupts registers), > 1 also delays setmaxnreg.inc by that many ns
+#endif
+
 template <typename R, int V, int B, int NB, int LY> struct MarchShape {
   static constexpr int BT = B / V;                 // threads per site
   static constexpr int SEG = 8 * NB;               // sites per line segment
@@ -214,7 +218,7 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB, LY>::NT, 1)
     // corrupted at random (a few wrong half spinors per launch on B200; tools/
     // stress_march.py), and keeping them resident for the whole kernel cost 18%.
     if (tid >= Sh::NC + 32) {
-      if constexpr (Sh::REALLOC) mbar_wait(regs_ok, 0);
+      if constexpr (Sh::REALLOC && !B200WD_MARCH_RACY) mbar_wait(regs_ok, 0);
       return;
     }
     if (tid != Sh::NC) return;  // idle lanes of the issuing warp: lanes leaving frees nothing
@@ -290,6 +294,7 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB, LY>::NT, 1)
 
   // ---------------- consumers ----------------
   if constexpr (Sh::REALLOC) {
+    if (B200WD_MARCH_RACY > 1) __nanosleep(B200WD_MARCH_RACY);  // experiment: let the idle warps exit first
     reg_inc<Sh::REG_C>();
     if ((tid & 31) == 0) mbar_arrive(regs_ok);
   }
