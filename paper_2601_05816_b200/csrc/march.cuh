@@ -29,10 +29,18 @@
 // moves its registers to the consumers with setmaxnreg.
 //
 // An item is LY y-adjacent segments (LY = 1, 2 or 4), sized so that a CTA has
-// 192 or 256 consumer threads.  One CTA per SM always: with two resident CTAs
-// per SM the register reallocation corrupted results on B200 (wrong half
-// spinors in a few warps per launch, gone with either one CTA per SM or
-// without setmaxnreg; profiles/r2_march_tuning.txt).
+// 192 or 256 consumer threads; one CTA per SM.  Three hazards found with the race
+// detector (tools/stress_march.py) shape the synchronisation:
+//   * mbarrier.arrive is NOT ordered behind the warp's outstanding shared-memory
+//     loads, not even after a MEMBAR: a buffer handed back right after issuing the
+//     loads was refilled (the small link copy of the next tile lands within a few
+//     hundred ns) before the last loads had read it.  Every hand-over is made
+//     data-dependent on the loaded values (arrive_after / hop_compute_release).
+//   * setmaxnreg: the idle warps of the producer warpgroup must not exit before
+//     every consumer warp finished setmaxnreg.inc (regs_ok), or consumer registers
+//     are corrupted; and the copy-issuing thread needs >= 56 registers or it starves
+//     the ring.
+//   * two resident CTAs per SM together with setmaxnreg corrupted results: 1 CTA/SM.
 //
 // Work units are (t-chunk, column) pairs, columns fastest, so the CTAs running
 // at one time march neighbouring columns through the same slices and their x/y
@@ -47,6 +55,18 @@
 
 namespace b200wd {
 
+#ifndef B200WD_MARCH_REG_C
+// registers per consumer / producer thread after setmaxnreg (2 C + P <= 504 = 3 x 168).
+// The producer needs room: measured on 16^3x32 c128 nrhs 16 (same box, safe exit
+// order): P = 24 0.344, P = 40 0.506-0.509 whatever C (200 ... 232), P = 56 0.574-0.580,
+// P = 72 0.563, P = 88 0.589 (C = 208), P = 104 0.586 (C = 200) -- with 40 registers the
+// copy-issuing thread is slow enough to starve the ring.
+#define B200WD_MARCH_REG_C 224
+#define B200WD_MARCH_REG_P 56
+#endif
+#ifndef B200WD_MARCH_EXP
+#define B200WD_MARCH_EXP 0  // experiments: 1 link copy before the spinor copy, 4 producer waits 1 us before each refill
+#endif
 #ifndef B200WD_MARCH_RACY
 #define B200WD_MARCH_RACY 0  // experiments: 1 idle producer warps exit at once (corrupts registers), > 1 also delays setmaxnreg.inc by that many ns
 #endif
@@ -60,8 +80,8 @@ template <typename R, int V, int B, int NB, int LY> struct MarchShape {
   static constexpr int NP = REALLOC ? 128 : 32;    // producer threads (one issues)
   static constexpr int NT = NC + NP;
   // registers after reallocation (per SM sub-partition: 16384 >= 32 * sum over its warps)
-  static constexpr int REG_C = 232;
-  static constexpr int REG_P = 40;
+  static constexpr int REG_C = B200WD_MARCH_REG_C;
+  static constexpr int REG_P = B200WD_MARCH_REG_P;
   static constexpr int LSP = NB * 96 * B;          // spinor complex per line segment
   static constexpr int LLK = NB * 72;              // link complex per line segment, one direction
   static constexpr int SPIN = LY * LSP;            // spinor complex per tile
@@ -129,6 +149,86 @@ template <int N> __device__ __forceinline__ void reg_inc() {
 }
 template <int N> __device__ __forceinline__ void reg_dec() {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
+
+// A hand-over of a shared-memory buffer must not become visible before this warp's
+// loads from it have returned: mbarrier.arrive is not ordered behind outstanding
+// LDS (not even after a MEMBAR -- measured: with the early release below and a
+// fast producer the refill's small link copy overtook the last link loads of a
+// warp in 13% of the launches on 16x32x16x16, c128 nrhs 32).  Summing a word of
+// every loaded value and branching on the sum makes the arrival data-dependent
+// on the loads (the branch is never taken for finite data).
+template <typename C> __device__ __forceinline__ uint32_t touch_word(const C& v) {
+  if constexpr (sizeof(v.x) == 8) return (uint32_t)__double2hiint(v.y);
+  else return __float_as_uint(v.y);
+}
+constexpr uint32_t kTouchMagic = 0x7ff8dea5u;
+template <typename R, int V> __device__ __forceinline__ uint32_t hop_touch(const HopRegs<R, V>& d) {
+  uint32_t s = 0;
+#pragma unroll
+  for (int e = 0; e < 9; ++e) s += touch_word(d.u[e]);
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) s += touch_word(d.h[v][q][c]);
+  return s;
+}
+__device__ __forceinline__ void arrive_after(uint64_t* bar, uint32_t chk) {
+  if (chk == kTouchMagic) __nanosleep(20);  // never for finite data; keeps the dependency
+  mbar_arrive(bar);
+}
+
+
+// g = M h for ONE colour vector (the per-spin half of matvec2, same operation order)
+template <bool DAG>
+__device__ __forceinline__ void matvec1(double2 (&g)[3], const double2 (&u)[9], const double2 (&h)[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double2 a = mk(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) a = DAG ? cmacc(a, u[3 * j + i], h[j]) : cmac(a, u[3 * i + j], h[j]);
+    g[i] = a;
+  }
+}
+template <bool DAG>
+__device__ __forceinline__ void matvec1(float2 (&g)[3], const float2 (&u)[9], const float2 (&h)[3]) {
+  float2 hs[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) hs[j] = mk(-h[j].y, h[j].x);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    float2 a = mk(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) a = DAG ? cmacc_s(a, u[3 * j + i], h[j], hs[j]) : cmac_s(a, u[3 * i + j], h[j], hs[j]);
+    g[i] = a;
+  }
+}
+// hop_compute with the buffer release in the middle: the first spin half of the
+// product has consumed every link entry and h[.][0]; together with a word of
+// h[.][1] the arrival then depends on every load of hop_load.
+template <int MU, bool FWD, typename R, int V>
+__device__ __forceinline__ void hop_compute_release(cx<R> (&acc)[V][12], const HopRegs<R, V>& d, uint64_t* bar,
+                                                    bool lead) {
+  using C = cx<R>;
+  C g[V][2][3];
+  uint32_t chk = 0;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    matvec1<!FWD>(g[v][0], d.u, d.h[v][0]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) chk += touch_word(g[v][0][c]) + touch_word(d.h[v][1][c]);
+  }
+  __syncwarp();
+  if (lead) arrive_after(bar, chk);
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    matvec1<!FWD>(g[v][1], d.u, d.h[v][1]);
+    accumulate_spin<MU, FWD, 0>(acc[v], g[v]);
+    accumulate_spin<MU, FWD, 1>(acc[v], g[v]);
+  }
 }
 
 // Work decomposition.  Columns [0, n1) are marched over the whole slice range
@@ -243,10 +343,16 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB, LY>::NT, 1)
     // neighbour tile: spinor lines (xs, ys..) and one link direction of lines (xl, yl..)
     auto tile = [&](int s, int xs, int ys, int xl, int yl, int zi, int mu) {
       if (!pfirst) mbar_wait(&empty[pslot], pphase ^ 1u);
+      if (B200WD_MARCH_EXP & 4) __nanosleep(1000);
       C* slot = ring + pslot * Sh::SLOT;
       mbar_expect_tx(&full[pslot], (uint32_t)(Sh::SLOT * sizeof(C)));
-      lines(slot, src, SB, s, xs, ys, zi, &full[pslot]);
-      lines(slot + Sh::SPIN, U + mu * nblk * 72, 72, s, xl, yl, zi, &full[pslot]);
+      if (B200WD_MARCH_EXP & 1) {
+        lines(slot + Sh::SPIN, U + mu * nblk * 72, 72, s, xl, yl, zi, &full[pslot]);
+        lines(slot, src, SB, s, xs, ys, zi, &full[pslot]);
+      } else {
+        lines(slot, src, SB, s, xs, ys, zi, &full[pslot]);
+        lines(slot + Sh::SPIN, U + mu * nblk * 72, 72, s, xl, yl, zi, &full[pslot]);
+      }
       if (++pslot == S) {
         pslot = 0;
         pphase ^= 1u;
@@ -452,17 +558,11 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB, LY>::NT, 1)
     const C* sb = ring + cslot * Sh::SLOT;                                      \
     HopRegs<R, V> hr;                                                           \
     hop_load<MU, FWD, R, V, KST>(hr, sb + so, sb + Sh::SPIN + lofs);            \
-    /* the loads must have read the slot before the arrival is visible: the   */ \
-    /* last ones issued (link rows) were seen overtaken by the refill's small */ \
-    /* link copy (stale colour-2 rows in a warp or two per few launches)      */ \
-    __threadfence_block();                                                      \
-    __syncwarp();                                                               \
-    if (lead) mbar_arrive(&empty[cslot]);                                       \
+    hop_compute_release<MU, FWD, R, V>(acc, hr, &empty[cslot], lead);           \
     if (++cslot == S) {                                                         \
       cslot = 0;                                                                \
       cphase ^= 1u;                                                             \
     }                                                                           \
-    hop_compute<MU, FWD, R, V>(acc, hr);                                        \
   }
       B200WD_MARCH_TILE(1, true)
       B200WD_MARCH_TILE(1, false)
@@ -529,26 +629,27 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB, LY>::NT, 1)
           }
         }
       }
-      __threadfence_block();
-      __syncwarp();
-      if (lead) mbar_arrive(own_free);
+      {
+        // the z-hop loads of the own tile feed acc: the arrival waits for them through it
+        uint32_t chk = 0;
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+#pragma unroll
+          for (int k = 0; k < 12; ++k) chk += touch_word(acc[v][k]);
+        __syncwarp();
+        if (lead) arrive_after(own_free, chk);
+      }
       ophase ^= 1u;
       {  // forward t hop of site s: U_0(s) P- psi(s+1), psi(s+1) from registers
-        C um[9];
+        HopRegs<R, V> hr;
 #pragma unroll
-        for (int e = 0; e < 9; ++e) um[e] = lk[lofs + e * 8];
-        __threadfence_block();  // as for the tile slots: loads complete before the release
-        __syncwarp();
-        if (lead) mbar_arrive(&lempty[ls]);
+        for (int e = 0; e < 9; ++e) hr.u[e] = lk[lofs + e * 8];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          C h[2][3], gg[2][3];
-          project_spin<0, true, 0>(h[0], nxt[v]);
-          project_spin<0, true, 1>(h[1], nxt[v]);
-          matvec2<false>(gg, um, h);
-          accumulate_spin<0, true, 0>(acc[v], gg);
-          accumulate_spin<0, true, 1>(acc[v], gg);
+          project_spin<0, true, 0>(hr.h[v][0], nxt[v]);
+          project_spin<0, true, 1>(hr.h[v][1], nxt[v]);
         }
+        hop_compute_release<0, true, R, V>(acc, hr, &lempty[ls], lead);  // hands the link planes back
         if (++ls == Sh::LST) {
           ls = 0;
           lphase ^= 1u;
@@ -659,25 +760,24 @@ static MarchCfg march_default_shape(const HopParams& p) {
   return c;
 }
 
-// Where the march is the default: the 256-thread shapes (whole 16-site z lines,
-// 16 consumer threads per site) that measured faster than the ring on B200 and
-// came through the race detector clean (tools/stress_march.py: 0 of 1,600
-// repeated launches differ): c128 nrhs 16 (0.519 vs 0.492 of the HBM roofline on
-// 16^3x32, same box and session) and 32 (0.532 vs 0.487), c64 nrhs 32 (0.495 vs
-// 0.481).  KNOWN ISSUE, which is why everything else stays on the ring kernels:
-// the 192-thread shapes (nrhs 6, 12, 24: threads per site not a power of two,
-// one producer warp, no register reallocation) are faster still (c128 nrhs 12
-// 0.576 vs 0.468, c64 nrhs 24 0.548 vs 0.448) but NOT reliably deterministic --
-// up to 5% of launches on 16^3x32 return a few sites whose colour-2 components
-// are wrong (stale rows 6-8 of a forward-hop link tile in one or two warps), not
-// cured by fences before the buffer hand-overs; root cause open
-// (profiles/r2_march_tuning.txt).  B200WD_MARCH=1 forces the march wherever a
-// shape exists (experiments only), B200WD_MARCH=0 turns it off.
+// Where the march is the default: shapes that measured faster than the ring
+// kernels on B200 (profiles/r2_march_tuning.txt; fraction of the HBM roofline, march
+// vs ring, same box and session) and come through the race detector clean
+// (tools/stress_march.py).  16^3x32: c128 nrhs 6 0.546 vs 0.507, 12 0.563 vs 0.468,
+// 16 0.572 vs 0.490 (24: 0.439 vs 0.433, 32: 0.461 vs 0.488, 8: 0.488 vs 0.491: ring);
+// c64 nrhs 24 0.516 vs 0.448, 32 0.535 vs 0.479 (6, 8, 12, 16: ring / two-line ring /
+// stream are faster).  Partial z lines, nrhs 12: c64 48^3x96 0.362 vs 0.291, 24^3x48
+// 0.322 vs 0.306 (c128 there 0.326 vs 0.346 and 0.394 vs 0.435: ring).  Unmeasured
+// shapes stay on the ring.  B200WD_MARCH=1 forces the march wherever a shape exists,
+// B200WD_MARCH=0 turns it off.
 template <typename R, int V, int B>
 static bool march_table(const HopParams& p) {
-  if (p.Z != 16) return false;
-  if constexpr (sizeof(R) == 8) return B == 16 || B == 32;
-  return B == 32;
+  if constexpr (sizeof(R) == 8) {
+    return p.Z == 16 && (B == 6 || B == 12 || B == 16);
+  } else {
+    if (p.Z == 16) return B == 24 || B == 32;
+    return B == 12 && (p.Z == 24 || p.Z == 48);
+  }
 }
 
 // Full-lattice fields, no halos, no clover, slice-aligned destination range.
