@@ -723,10 +723,9 @@ __global__ void B200WD_RING_BOUNDS(RingShape<R, V, B, NB, PAR>::NT) hop_ring_ker
     else if (ring_early_release<R, B>()) {                                                           \
       HopRegs<R, V> hr;                                                                              \
       hop_load<((H) >> 1), !((H)&1), R, V, KST>(hr, sb + j * 96 * B + lo * B + r0, sb + Sh::SPIN + lofs); \
-      __syncwarp();                                                                                  \
-      if (lead) mbar_arrive(&empty[slot]);                                                           \
+      /* release in the middle of the product, data-dependent on every load (stencil.cuh) */        \
+      hop_compute_release<((H) >> 1), !((H)&1), R, V>(acc, hr, &empty[slot], lead);                  \
       released = true;                                                                               \
-      hop_compute<((H) >> 1), !((H)&1), R, V>(acc, hr);                                              \
     } else if (!B200WD_RING_NOMATH)                                                                  \
       hop_full<((H) >> 1), !((H)&1), R, V, true, true>(acc, sb + j * 96 * B + lo * B + r0, KST,      \
                                                         sb + Sh::SPIN + lofs, 8);                    \

@@ -152,85 +152,6 @@ template <int N> __device__ __forceinline__ void reg_dec() {
 }
 
 
-// A hand-over of a shared-memory buffer must not become visible before this warp's
-// loads from it have returned: mbarrier.arrive is not ordered behind outstanding
-// LDS (not even after a MEMBAR -- measured: with the early release below and a
-// fast producer the refill's small link copy overtook the last link loads of a
-// warp in 13% of the launches on 16x32x16x16, c128 nrhs 32).  Summing a word of
-// every loaded value and branching on the sum makes the arrival data-dependent
-// on the loads (the branch is never taken for finite data).
-template <typename C> __device__ __forceinline__ uint32_t touch_word(const C& v) {
-  if constexpr (sizeof(v.x) == 8) return (uint32_t)__double2hiint(v.y);
-  else return __float_as_uint(v.y);
-}
-constexpr uint32_t kTouchMagic = 0x7ff8dea5u;
-template <typename R, int V> __device__ __forceinline__ uint32_t hop_touch(const HopRegs<R, V>& d) {
-  uint32_t s = 0;
-#pragma unroll
-  for (int e = 0; e < 9; ++e) s += touch_word(d.u[e]);
-#pragma unroll
-  for (int v = 0; v < V; ++v)
-#pragma unroll
-    for (int q = 0; q < 2; ++q)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) s += touch_word(d.h[v][q][c]);
-  return s;
-}
-__device__ __forceinline__ void arrive_after(uint64_t* bar, uint32_t chk) {
-  if (chk == kTouchMagic) __nanosleep(20);  // never for finite data; keeps the dependency
-  mbar_arrive(bar);
-}
-
-
-// g = M h for ONE colour vector (the per-spin half of matvec2, same operation order)
-template <bool DAG>
-__device__ __forceinline__ void matvec1(double2 (&g)[3], const double2 (&u)[9], const double2 (&h)[3]) {
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    double2 a = mk(0.0, 0.0);
-#pragma unroll
-    for (int j = 0; j < 3; ++j) a = DAG ? cmacc(a, u[3 * j + i], h[j]) : cmac(a, u[3 * i + j], h[j]);
-    g[i] = a;
-  }
-}
-template <bool DAG>
-__device__ __forceinline__ void matvec1(float2 (&g)[3], const float2 (&u)[9], const float2 (&h)[3]) {
-  float2 hs[3];
-#pragma unroll
-  for (int j = 0; j < 3; ++j) hs[j] = mk(-h[j].y, h[j].x);
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    float2 a = mk(0.f, 0.f);
-#pragma unroll
-    for (int j = 0; j < 3; ++j) a = DAG ? cmacc_s(a, u[3 * j + i], h[j], hs[j]) : cmac_s(a, u[3 * i + j], h[j], hs[j]);
-    g[i] = a;
-  }
-}
-// hop_compute with the buffer release in the middle: the first spin half of the
-// product has consumed every link entry and h[.][0]; together with a word of
-// h[.][1] the arrival then depends on every load of hop_load.
-template <int MU, bool FWD, typename R, int V>
-__device__ __forceinline__ void hop_compute_release(cx<R> (&acc)[V][12], const HopRegs<R, V>& d, uint64_t* bar,
-                                                    bool lead) {
-  using C = cx<R>;
-  C g[V][2][3];
-  uint32_t chk = 0;
-#pragma unroll
-  for (int v = 0; v < V; ++v) {
-    matvec1<!FWD>(g[v][0], d.u, d.h[v][0]);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) chk += touch_word(g[v][0][c]) + touch_word(d.h[v][1][c]);
-  }
-  __syncwarp();
-  if (lead) arrive_after(bar, chk);
-#pragma unroll
-  for (int v = 0; v < V; ++v) {
-    matvec1<!FWD>(g[v][1], d.u, d.h[v][1]);
-    accumulate_spin<MU, FWD, 0>(acc[v], g[v]);
-    accumulate_spin<MU, FWD, 1>(acc[v], g[v]);
-  }
-}
-
 // Work decomposition.  Columns [0, n1) are marched over the whole slice range
 // by one unit each (n1 is a multiple of the grid: whole rounds in which every
 // CTA carries one column through the same slices); the remaining ncol - n1
