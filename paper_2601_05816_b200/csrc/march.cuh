@@ -159,6 +159,7 @@ template <int N> __device__ __forceinline__ void reg_dec() {
 // Units are ordered (chunk, column): the CTAs running at one time march
 // neighbouring columns through the same slices.
 struct MarchGrid {
+  int32_t px, py;   // column patch (x, y items) of the traversal; 0: natural order
   int32_t lz, ny;   // segments per z line, lines in y
   int64_t ncol;     // X * ny * lz
   int32_t ta, nT;   // destination slices [ta, ta + nT)
@@ -182,8 +183,18 @@ __device__ __forceinline__ TsUnit march_decode(int64_t u, const MarchGrid& g) {
   }
   w.zi = (int)(c % (uint32_t)g.lz);
   c /= (uint32_t)g.lz;
-  w.y = (int)(c % (uint32_t)g.ny);
-  w.x = (int)(c / (uint32_t)g.ny);
+  if (g.px == 0) {
+    w.y = (int)(c % (uint32_t)g.ny);
+    w.x = (int)(c / (uint32_t)g.ny);
+  } else {
+    // patched order: all columns of one px x py patch before the next patch, so the
+    // CTAs of a round cover a compact x-y region and find their x and y neighbours in L2
+    const uint32_t pa = (uint32_t)(g.px * g.py);
+    const uint32_t within = c % pa, patch = c / pa;
+    const uint32_t npy = (uint32_t)(g.ny / g.py);
+    w.x = (int)((patch / npy) * g.px + within / g.py);
+    w.y = (int)((patch % npy) * g.py + within % g.py);
+  }
   return w;
 }
 
@@ -634,6 +645,40 @@ static bool launch_march_kernel(const HopParams& p, const MarchGrid& g0, int S, 
     g.nch2 = g.ncol > g.n1 ? ts_choose_nch(g.ncol - g.n1, g.nT, grid_max, 5) : 1;
   }
   g.n_units = g.n1 + (g.ncol - g.n1) * g.nch2;
+  // Column patches when a round of the grid covers less than two x rows (then the x
+  // neighbours of most columns belong to other rounds and miss L2: 48^3x96): the patch
+  // px | X, py | ny with px * py * lz <= grid and the smallest perimeter / area.
+  // B200WD_MARCH_PATCH="px,py" forces a patch, "0,0" turns patching off.
+  g.px = g.py = 0;
+  {
+    static int fx = -1, fy = -1;
+    if (fx < 0) {
+      fx = fy = -2;
+      const char* e = getenv("B200WD_MARCH_PATCH");
+      if (e) sscanf(e, "%d,%d", &fx, &fy);
+    }
+    if (fx > 0 && fy > 0) {
+      if (p.X % fx == 0 && g.ny % fy == 0) {
+        g.px = fx;
+        g.py = fy;
+      }
+    } else if (fx != 0 && (int64_t)g.ny * g.lz * 2 > grid_max) {
+      double best = 1e30;
+      for (int px = 1; px <= p.X; ++px) {
+        if (p.X % px) continue;
+        for (int py = 1; py <= g.ny; ++py) {
+          if (g.ny % py || (int64_t)px * py * g.lz > grid_max) continue;
+          const double perim = 1.0 / px + 1.0 / py;
+          if (perim < best - 1e-12) {
+            best = perim;
+            g.px = px;
+            g.py = py;
+          }
+        }
+      }
+      if (g.px == p.X && g.py == g.ny) g.px = g.py = 0;
+    }
+  }
   const int64_t grid = grid_max < g.n_units ? grid_max : g.n_units;
   hop_march_kernel<R, V, B, NB, LY, ZG><<<(unsigned)grid, Sh::NT, smem, st>>>(p, g, S);
   return true;

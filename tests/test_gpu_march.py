@@ -16,7 +16,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
-# (B200WD_MARCH_CFG "NB,LY,S,NCH" or "" for the default shape, lattices T x X x Y x Z, rhs counts)
+# (B200WD_MARCH_CFG "NB,LY,S,NCH" or "" for the default shape [+ "|px,py" column patch], lattices, rhs counts)
 CASES = [
     ("", "4x4x4x16,6x2x4x32", "6,8,12,16,32"),      # default shapes: whole lines, 1/2/4 y lines per item
     ("", "8x16x12x16", "12,16,32"),                  # more columns than CTAs: whole columns + chunked rest
@@ -26,14 +26,18 @@ CASES = [
     ("2,2,0,3", "8x4x6x16,6x2x2x32", "8,12"),        # two y lines, 3 chunks (wrap-around y tiles)
     ("1,4,0,0", "4x2x4x24,4x16x12x16", "8"),         # four y lines
     ("2,1,2,1", "4x4x4x16", "12,16"),                # ring depth 2, one chunk
+    ("|2,2", "4x4x4x16,6x4x8x24", "12,16"),          # patched column order (B200WD_MARCH_PATCH)
 ]
 
 
 @pytest.mark.parametrize("cfg,dims,bs", CASES)
 def test_march_shape_matches_oracle(cfg, dims, bs):
     env = dict(os.environ, B200WD_MARCH="1")
+    cfg, _, patch = cfg.partition("|")
     if cfg:
         env["B200WD_MARCH_CFG"] = cfg
+    if patch:
+        env["B200WD_MARCH_PATCH"] = patch
     r = subprocess.run([sys.executable, str(ROOT / "tests" / "helpers" / "tstream_check.py"), dims, bs], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
