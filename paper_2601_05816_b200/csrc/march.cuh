@@ -756,6 +756,9 @@ static bool try_launch_march(const HopParams& p, cudaStream_t st) {
   if (p.d_begin % p.per_t || p.d_end % p.per_t || p.d_end <= p.d_begin) return false;
   const MarchCfg e = march_env();
   if (mode != 1 && e.nb <= 0 && !march_table<R, V, B>(p)) return false;
+  // short slice ranges (the T chunks of the host-pipelined apply, thin T-split interiors):
+  // a unit re-reads two own tiles whatever its length, so the ring serves ranges under 8 slices
+  if (mode != 1 && e.nb <= 0 && (p.d_end - p.d_begin) / p.per_t < 8) return false;
   MarchCfg c = march_default_shape<R, V, B>(p);
   if (e.nb > 0) {
     c.nb = e.nb;
