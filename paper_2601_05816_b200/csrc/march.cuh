@@ -67,6 +67,10 @@ namespace b200wd {
 #ifndef B200WD_MARCH_EXP
 #define B200WD_MARCH_EXP 0  // experiments: 1 link copy before the spinor copy, 4 producer waits 1 us before each refill
 #endif
+#ifndef B200WD_MARCH_LD0
+#define B200WD_MARCH_LD0 4  // psi(s+1) loads before the x+ tile / before the x- tile (the rest before y+)
+#define B200WD_MARCH_LD1 4
+#endif
 #ifndef B200WD_MARCH_RACY
 #define B200WD_MARCH_RACY 0  // experiments: 1 idle producer warps exit at once (corrupts registers), > 1 also delays setmaxnreg.inc by that many ns
 #endif
@@ -474,16 +478,22 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB, LY>::NT, 1)
           matvec2<true>(carry[v], um, h);
         }
       }
-      {  // psi(s+1) into the registers psi(s) just left
-        const C* pn = src + elem(wrapi(s + 1, p.T));
+      // psi(s+1) into the registers psi(s) just left, in three batches (before the x+,
+      // x- and y+ tiles): twelve 128-bit loads at once throttle the shared-memory loads of
+      // the first tile hop behind them (MIO queue); B200WD_MARCH_LD0/1 = batch sizes
+      const C* pn = src + elem(wrapi(s + 1, p.T));
+      auto load_next = [&](int k0, int k1) {
 #pragma unroll
         for (int k = 0; k < 12; ++k) {
-          C t1[V];
-          PinLd<R, V>::ld(t1, pn + k * KST);
+          if (k >= k0 && k < k1) {
+            C t1[V];
+            PinLd<R, V>::ld(t1, pn + k * KST);
 #pragma unroll
-          for (int v = 0; v < V; ++v) nxt[v][k] = t1[v];
+            for (int v = 0; v < V; ++v) nxt[v][k] = t1[v];
+          }
         }
-      }
+      };
+      load_next(0, B200WD_MARCH_LD0);
 #define B200WD_MARCH_TILE(MU, FWD)                                              \
   {                                                                             \
     mbar_wait(&full[cslot], cphase);                                            \
@@ -497,7 +507,9 @@ __global__ void __launch_bounds__(MarchShape<R, V, B, NB, LY>::NT, 1)
     }                                                                           \
   }
       B200WD_MARCH_TILE(1, true)
+      load_next(B200WD_MARCH_LD0, B200WD_MARCH_LD0 + B200WD_MARCH_LD1);
       B200WD_MARCH_TILE(1, false)
+      load_next(B200WD_MARCH_LD0 + B200WD_MARCH_LD1, 12);
       B200WD_MARCH_TILE(2, true)
       mbar_wait(own_full, ophase);  // the own tile is complete (every warp stored its part at the top of the step)
       {  // z hops, receiver side (U_3 in the second link plane)
