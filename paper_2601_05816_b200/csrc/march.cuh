@@ -741,19 +741,19 @@ static MarchCfg march_default_shape(const HopParams& p) {
 // Where the march is the default: shapes that measured faster than the ring
 // kernels on B200 (profiles/r2_march_tuning.txt; fraction of the HBM roofline, march
 // vs ring, same box and session) and come through the race detector clean
-// (tools/stress_march.py).  16^3x32: c128 nrhs 6 0.546 vs 0.507, 12 0.563 vs 0.468,
-// 16 0.572 vs 0.490 (24: 0.439 vs 0.433, 32: 0.461 vs 0.488, 8: 0.488 vs 0.491: ring);
-// c64 nrhs 24 0.516 vs 0.448, 32 0.535 vs 0.479 (6, 8, 12, 16: ring / two-line ring /
-// stream are faster).  Partial z lines, nrhs 12: c64 48^3x96 0.362 vs 0.291, 24^3x48
-// 0.322 vs 0.306 (c128 there 0.326 vs 0.346 and 0.394 vs 0.435: ring).  Unmeasured
-// shapes stay on the ring.  B200WD_MARCH=1 forces the march wherever a shape exists,
-// B200WD_MARCH=0 turns it off.
+// (tools/stress_march.py).  16^3x32: c128 nrhs 6 0.575 vs 0.507, 8 0.502 vs 0.492,
+// 12 0.590 vs 0.468, 16 0.601 vs 0.490, 24 0.447 vs 0.438 (32: 0.466 vs 0.489, 4: 0.466
+// vs 0.530: ring); c64 nrhs 12 0.414 vs 0.403, 24 0.506 vs 0.448, 32 0.576 vs 0.479
+// (6, 8, 16: ring / two-line ring / stream are faster).  Partial z lines, nrhs 12:
+// c64 48^3x96 0.365 vs 0.291, 24^3x48 0.330 vs 0.306 (c128 there 0.341 vs 0.346 and
+// 0.394 vs 0.435: ring).  Unmeasured shapes stay on the ring.  B200WD_MARCH=1 forces
+// the march wherever a shape exists, B200WD_MARCH=0 turns it off.
 template <typename R, int V, int B>
 static bool march_table(const HopParams& p) {
   if constexpr (sizeof(R) == 8) {
-    return p.Z == 16 && (B == 6 || B == 12 || B == 16);
+    return p.Z == 16 && (B == 6 || B == 8 || B == 12 || B == 16 || B == 24);
   } else {
-    if (p.Z == 16) return B == 24 || B == 32;
+    if (p.Z == 16) return B == 12 || B == 24 || B == 32;
     return B == 12 && (p.Z == 24 || p.Z == 48);
   }
 }
