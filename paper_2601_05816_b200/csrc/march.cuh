@@ -13,8 +13,9 @@
 // rhs) as in the ring.  The thread keeps the t window of its own site in
 // REGISTERS:
 //   * psi(s+1) is loaded straight from global memory into registers (one
-//     128-bit load per component, coalesced across the warp) at the start of
-//     step s and lands while the other six hops are computed; it feeds the
+//     128-bit load per component, coalesced across the warp; three batches of
+//     four during the first tile hops of step s, pinned with ld.volatile) and
+//     lands while the other hops are computed; it feeds the
 //     forward t hop of site s at the end of the step and stays in registers as
 //     the own spinor of step s+1 (self term, z hops via a shared-memory copy);
 //   * the backward t hop of site s+1, U_0(s)^H P+ psi(s), is finished at step
